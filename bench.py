@@ -1,0 +1,369 @@
+"""MoE-layer benchmark (BASELINE.json metric: MoE-layer tokens/sec at 1/2/4/8
+B200 and % of roofline).
+
+A step = one forward + backward of the MoE layer (gate GEMM, routing,
+dispatch, EP all-to-all, expert FFN, all-to-all back, combine, and the
+backward of all of it incl. weight gradients) over T tokens per GPU of
+synthetic SplitMix64 data.  Workload = config c2 (BASELINE.json configs[1]):
+Switch top-1, E = 64, d = 1024, d_ff = 4096, T = 65536 tokens/GPU, bf16,
+experts sharded over the N GPUs (weak scaling).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config c2]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+--impl reference times the reference's CPU implementation of the path on the
+host cores: the reference has no MoE-layer arithmetic, so this is the CPU
+oracle restatement (oracle/, kind "port") on a bounded token sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer tokens/sec at 1/2/4/8 B200; % of HBM/tensor/NVLink roofline"
+
+CONFIGS = {
+    "c1": dict(E=8, k=2, d=512, dff=2048, T=4096, cf=1.25, dtype="f32",
+               desc="c1: E=8 top-2 MoE FFN layer, d=512, d_ff=2048, T=4096, cf=1.25, fp32 fwd+bwd"),
+    "c2": dict(E=64, k=1, d=1024, dff=4096, T=65536, cf=1.25, dtype="bf16",
+               desc="c2: Switch top-1 MoE layer fwd+bwd, E=64, d=1024, d_ff=4096 (4d), "
+                    "T=65536 tokens/GPU, cf=1.25, bf16, experts sharded E/N per GPU"),
+    "c3": dict(E=32, k=2, d=1024, dff=4096, T=65536, cf=1.25, dtype="bf16", skew=1.2,
+               desc="c3: E=32 top-2, Zipf-skewed gate bias -1.2*ln(e+1), capacity drops, "
+                    "d=1024, d_ff=4096, T=65536/GPU, bf16 fwd+bwd"),
+    "c4": dict(E=64, k=2, d=4096, dff=16384, T=16384, cf=1.25, dtype="bf16",
+               desc="c4: GPT-MoE block d=4096, d_ff=16384, E=64 top-2, T=16384/GPU, bf16 fwd+bwd"),
+}
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+         "source": "fallback (B200_PROFILING.md)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            m = json.load(f)
+        for key in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained"):
+            if key in m:
+                p[key] = float(m[key])
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) >= 8:
+                for n, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------ CPU arm --
+def cpu_oracle_tokens_per_s(cfg, tokens, seed=2205, repeats=1):
+    """Oracle fwd+bwd of the layer on `tokens` tokens (all host threads)."""
+    import numpy as np
+
+    import oracle
+    E, k, d, dff, cf = cfg["E"], cfg["k"], cfg["d"], cfg["dff"], cfg["cf"]
+    bf16 = cfg["dtype"] == "bf16"
+    t = oracle.make_layer_tensors(seed, tokens, d, dff, E, bf16)
+    bg = None
+    if cfg.get("skew"):
+        bg = np.array([-cfg["skew"] * np.log(e + 1.0) for e in range(E)], np.float32)
+    C = int(np.ceil(k * cf * tokens / E))
+    best = None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        fwd = oracle.moe_forward(t["x"], t["wg"], bg, t["w1"], t["b1"], t["w2"], t["b2"], k, C, bf16)
+        fwd["logits_used"] = fwd["logits"]
+        oracle.moe_backward(t["x"], t["wg"], bg, t["w1"], t["b1"], t["w2"], t["b2"], k, C, bf16,
+                            fwd, t["dy"], 0.01)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return tokens / best, best
+
+
+def cpu_sample_tokens(cfg):
+    # ~10-30 s of host work: per-token oracle cost ~ 16 * k * d * dff flops (fp64)
+    per_token = 16.0 * cfg["k"] * cfg["d"] * cfg["dff"]
+    return int(max(64, min(cfg["T"], 1.0e11 / per_token)) // 64 * 64)
+
+
+def run_reference_arm(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    n = cpu_sample_tokens(cfg) // 4 if args.steps > 1 else cpu_sample_tokens(cfg)
+    n = max(64, n // 64 * 64)
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_oracle_tokens_per_s(cfg, 64)
+    times = []
+    for _ in range(args.steps):
+        _, dt = cpu_oracle_tokens_per_s(cfg, n)
+        times.append(dt)
+    value = n * len(times) / sum(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * sum(times) / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64-accumulate",
+        "data": "synthetic (SplitMix64-seeded, rng.hpp)",
+        "config": {"workload": cfg["desc"], "sample_tokens_per_step": n},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": oracle.num_threads(),
+                         "kind": "port",
+                         "sample": f"{n} tokens of {cfg['desc'].split(':')[0]} per step "
+                                   "(oracle/moe_oracle.c fwd+bwd; the reference itself has no "
+                                   "MoE-layer arithmetic, SPEC.md:15,153,156)"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--tokens", type=int, default=0, help="override T (tokens per GPU)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--phases", action="store_true", help="print a per-phase breakdown line")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.tokens:
+        cfg["T"] = args.tokens
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2205_10034_b200 import EPGroup, MoEConfig, MoELayer, kernel_launch_count
+    from paper_2205_10034_b200.layer import T_DY
+
+    ws, rank, local = dist_env()
+    assert args.gpus == ws or ws == 1, "--gpus must match WORLD_SIZE"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ep = None
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        ep = EPGroup(ws, rank)
+    dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+    E, k, d, dff, T, cf = cfg["E"], cfg["k"], cfg["d"], cfg["dff"], cfg["T"], cfg["cf"]
+    mcfg = MoEConfig(E, k, d, dff, cf, T, dtype, gate_bias=bool(cfg.get("skew")))
+    layer = MoELayer(mcfg, ep=ep, device=dev)
+    gb = None
+    if cfg.get("skew"):
+        import math
+        gb = torch.tensor([-cfg["skew"] * math.log(e + 1.0) for e in range(E)],
+                          dtype=torch.float32, device=dev)
+    layer.init_params(1234, gate_bias=gb)
+    x = layer.make_input(1234)
+    dy = layer.make_input(1234, T_DY)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        layer.forward(x)
+        layer.backward(dy, d_aux=0.01)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-timed region: exactly K steps, inputs resident in HBM ----
+    sampler = ClockSampler(local)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    sampler.start()
+    n0 = kernel_launch_count()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    barrier()
+    launches = kernel_launch_count() - n0
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+
+    # ---- separate profiled pass: per-phase CUDA events on the launch stream ----
+    layer.set_profiling(True)
+    phase_tot = {}
+    for _ in range(args.steps):
+        layer.forward(x)
+        for n, v in layer.phase_times().items():
+            phase_tot["fwd." + n] = phase_tot.get("fwd." + n, 0.0) + v
+        layer.backward(dy, d_aux=0.01)
+        for n, v in layer.phase_times().items():
+            phase_tot["bwd." + n] = phase_tot.get("bwd." + n, 0.0) + v
+    layer.set_profiling(False)
+    barrier()
+    t_ms = torch.tensor([ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms = float(t_ms.item())
+    ms_step = ms / args.steps
+    value = ws * T * args.steps / (ms / 1000.0)
+
+    # routing statistics of the last step
+    _, rout = layer.forward(x, routing=True)
+    torch.cuda.synchronize()
+    kept_local = int(rout["kept"].sum().item())
+    count1 = rout["count1"].float()
+    imb = float(count1.max().item() / max(count1.mean().item(), 1e-9))
+    drop = 1.0 - kept_local / float(T * k)
+
+    # ---- roofline of the dominant kernel (expert grouped GEMMs, tcgen05) ----
+    pk = peaks()
+    gemm_phases = ["fwd.ffn1", "fwd.ffn2", "bwd.dgrad_ffn2", "bwd.dgrad_ffn1", "bwd.wgrad_w1",
+                   "bwd.wgrad_w2"]
+    gemm_ms = sum(phase_tot.get(p, 0.0) for p in gemm_phases) / args.steps
+    # algorithmic flops per step on this GPU: rows the local experts processed
+    kept_t = torch.tensor([kept_local], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(kept_t)
+    rows_local = float(kept_t.item()) / ws  # EP: on average each GPU computes T*k kept rows
+    flops_step = 6 * 2.0 * rows_local * d * dff
+    achieved_tf = flops_step / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
+    prof_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    traffic = None
+    if os.path.exists(prof_path):
+        with open(prof_path) as f:
+            traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
+    roof = {"kernel": "tc_gemm_kernel (6 expert GEMMs/step: ffn1, ffn2, 2x dgrad, 2x wgrad)",
+            "bound": "tensor", "achieved": achieved_tf, "peak": pk["bf16_tflops_sustained"],
+            "unit": "TFLOP/s", "frac": (achieved_tf / pk["bf16_tflops_sustained"]) if achieved_tf else None,
+            "traffic": traffic, "peak_source": pk["source"] + ", sustained",
+            "flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
+            "gemm_share_of_step": gemm_ms / ms_step if ms_step else None}
+
+    # ---- end to end through the host-buffer API (H2D + step + D2H) ----
+    e2e = None
+    if not args.no_e2e:
+        xh = x.cpu().pin_memory()
+        dyh = dy.cpu().pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        dxh = torch.empty_like(xh).pin_memory()
+        layer.train_step_host(xh, dyh, yh, dxh, d_aux=0.01)
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            layer.train_step_host(xh, dyh, yh, dxh, d_aux=0.01)
+        ev1.record(stream)
+        barrier()
+        e_ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
+        if ws > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e_ms = float(e_ms.item())
+        nbytes = T * d * (2 if dtype == torch.bfloat16 else 4)
+        e2e = {"value": ws * T * args.steps / (e_ms / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
+               "ms_per_step": e_ms / args.steps,
+               "api": "moe_layer_train_step_host (pinned x, dy -> y, dx)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        import oracle
+        n = cpu_sample_tokens(cfg)
+        v, dt = cpu_oracle_tokens_per_s(cfg, n)
+        cpu = {"value": v, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "port",
+               "sample": f"{n} tokens of the {args.config} layer fwd+bwd ({dt:.1f} s, "
+                         "oracle/moe_oracle.c fp64-accumulate, OpenMP)"}
+
+    a2a_ms = sum(v for n, v in phase_tot.items() if ".a2a" in n) / args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"],
+        "data": "synthetic (SplitMix64-seeded x, dy and weights; rng.hpp substreams)",
+        "config": {"workload": cfg["desc"], "tokens_per_gpu": T, "experts": E, "top_k": k,
+                   "d_model": d, "d_ff": dff, "capacity_factor": cf,
+                   "capacity": layer.capacity, "experts_per_gpu": E // ws,
+                   "parallelism": f"ep{ws}" if ws > 1 else "single",
+                   "l2": "inputs larger than L2 (x 128 MiB + weights 1 GiB per step), no flush"},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks,
+        "routing": {"imbalance_ratio": imb, "drop_rate": drop},
+        "a2a_ms_per_step": a2a_ms if ws > 1 else 0.0,
+        "phases_ms_per_step": {n: v / args.steps for n, v in sorted(phase_tot.items())},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ep is not None:
+        layer.close()
+        ep.close()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

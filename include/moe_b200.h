@@ -1,0 +1,340 @@
+/*
+ * moe_b200.h — C-ABI of the B200-native SE-MoE MoE-layer hot path.
+ *
+ * The reference (`/root/reference/proj`, "moesim") exposes its path only as the
+ * C++ library target moesim::core (core/CMakeLists.txt:3-25) with value-type
+ * signatures and C++ exceptions.  This header is the drop-in boundary:
+ *
+ *   1. moesim_* — byte/bit-exact equivalents of the reference functions that
+ *      exist on the path, executed on the GPU, with host buffers in and out
+ *      (the reference's calling convention).  The C++ wrappers in
+ *      include/moesim_b200.hpp restore the reference's exact signatures and
+ *      exception types.
+ *   2. moe_*    — the performance path on device pointers (the MoE-layer operator
+ *      the reference does not have).
+ *
+ * Conventions:
+ *   - every call returns moe_status_t; moe_last_error() returns the thread-local
+ *     message of the last failing call in the reference's "<field>: <reason>"
+ *     form;
+ *   - MOE_ERR_INVALID_ARGUMENT <-> std::invalid_argument,
+ *     MOE_ERR_OUT_OF_RANGE <-> std::out_of_range, MOE_ERR_CONFIG <->
+ *     moesim::ConfigError, MOE_ERR_LOGIC <-> std::logic_error;
+ *   - device calls enqueue on the caller's stream (cudaStream_t passed as void*)
+ *     and never synchronise the host unless documented;
+ *   - the caller owns activations and parameters; a handle owns its workspaces.
+ *   - no torch types, plain pointers and sizes only.
+ */
+#ifndef MOE_B200_H_
+#define MOE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOE_ABI_VERSION 1
+
+typedef enum moe_status {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument  (collectives.cpp:11-13)      */
+  MOE_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range      (topology.cpp:48,62-63)       */
+  MOE_ERR_CONFIG = 3,           /* moesim::ConfigError    (types.hpp:24-26)             */
+  MOE_ERR_LOGIC = 4,            /* std::logic_error       (sim_engine.cpp:31)           */
+  MOE_ERR_CUDA = 5,
+  MOE_ERR_NCCL = 6
+} moe_status_t;
+
+typedef enum moe_dtype { MOE_DTYPE_F32 = 0, MOE_DTYPE_BF16 = 1 } moe_dtype_t;
+
+const char* moe_last_error(void);
+int moe_abi_version(void);
+/* Number of kernels this library launched since load (all entry points). */
+uint64_t moe_kernel_launch_count(void);
+
+/* ======================================================================
+ * 1. moesim compatibility layer (host buffers, device execution)
+ * ====================================================================== */
+
+/* moesim::SliceIndexEntry (collectives.hpp:60-66). */
+typedef struct moe_slice_index_entry {
+  uint64_t slice_id;
+  uint64_t offset;
+  uint64_t length;
+} moe_slice_index_entry_t;
+
+/* moesim::alltoall_flat (collectives.hpp:36, collectives.cpp:10-21):
+ * out[i][j] = in[j][i].  The R x R chunk matrix is flattened row-major
+ * [src][dst]: lens[n_chunks], data = concatenation in that order; the output
+ * uses the same convention.  n_chunks != ranks*ranks -> INVALID_ARGUMENT
+ * ("alltoall: payload is not a square rank matrix"). */
+moe_status_t moesim_alltoall_flat(uint64_t ranks, uint64_t n_chunks, const uint64_t* lens,
+                                  const uint8_t* data, uint64_t* out_lens, uint8_t* out_data);
+
+/* moesim::fuse_slices (collectives.hpp:78, collectives.cpp:88-98). n == 0 ->
+ * INVALID_ARGUMENT ("fuse_slices: empty slice list"). blob gets sum(lens). */
+moe_status_t moesim_fuse_slices(uint64_t n, const uint64_t* lens, const uint8_t* data,
+                                uint8_t* blob, moe_slice_index_entry_t* index);
+
+/* moesim::split_blob (collectives.hpp:79, collectives.cpp:100-118): validates
+ * contiguity + coverage (INVALID_ARGUMENT otherwise), writes the slices back to
+ * back into out (sum of lengths == blob_len bytes). */
+moe_status_t moesim_split_blob(uint64_t blob_len, const uint8_t* blob, uint64_t n,
+                               const moe_slice_index_entry_t* index, uint8_t* out);
+
+/* moesim::gen_trace (workload.hpp:41-42, workload.cpp:19-53): counts is
+ * uint64 [steps][ranks][experts]. experts == 0 or skew < 0 -> CONFIG. */
+moe_status_t moesim_gen_trace(uint64_t seed, uint32_t steps, uint32_t ranks, uint32_t experts,
+                              uint64_t tokens_per_rank, double skew, uint64_t* counts);
+
+/* moesim::imbalance_ratio (workload.hpp:46, workload.cpp:55-66); zero tokens
+ * -> CONFIG ("imbalance_ratio: trace carries zero tokens"). */
+moe_status_t moesim_imbalance_ratio(uint32_t steps, uint32_t ranks, uint32_t experts,
+                                    const uint64_t* counts, double* out);
+
+/* moesim::build_schedule (ring_offload.hpp:45, ring_offload.cpp:31-50).
+ * ops: int64 [n][4] = (kind 0=load 1=compute 2=release, layer, slot,
+ * waits_release_of or -1); capacity must be >= 3*layers + min(slots, layers).
+ * ring_slots == 0 or layers == 0 -> CONFIG. */
+moe_status_t moesim_ring_build_schedule(uint32_t layers, uint32_t ring_slots, int64_t* ops,
+                                        uint64_t capacity, uint64_t* n_ops, uint32_t* slots,
+                                        int* clamped);
+
+/* ======================================================================
+ * 2. device data-plane ops (device pointers, caller's stream)
+ * ====================================================================== */
+
+/* Fill out[i] = lo + (hi-lo) * u_i with u_i the i-th SplitMix64(seed) draw
+ * (rng.hpp:23-32), rounded to dtype.  Bit-identical to the sequential stream. */
+moe_status_t moe_fill_uniform(void* out, uint64_t n, moe_dtype_t dtype, uint64_t seed, double lo,
+                              double hi, void* stream);
+
+/* Device gen_trace: counts (uint64, zeroed by the call) [steps][ranks][experts]. */
+moe_status_t moe_gen_trace_device(uint64_t seed, uint32_t steps, uint32_t ranks, uint32_t experts,
+                                  uint64_t tokens_per_rank, double skew, uint64_t* counts,
+                                  void* stream);
+
+/* Single-device R x R ragged transpose (alltoall_flat with the ranks emulated
+ * on one GPU): chunk (s,d) of length lens[s*R+d] at in + in_off[s*R+d] goes to
+ * out + out_off[d*R+s].  Offsets/lengths are device arrays. */
+moe_status_t moe_alltoall_flat_device(uint64_t ranks, const uint64_t* lens, const uint64_t* in_off,
+                                      const uint8_t* in, const uint64_t* out_off, uint8_t* out,
+                                      void* stream);
+
+/* Fusion packing on the device: n slices (device pointer table) -> one blob;
+ * index (device, n entries) = (i, exclusive prefix of lens, lens). */
+moe_status_t moe_fuse_slices_device(uint64_t n, const uint8_t* const* slices, const uint64_t* lens,
+                                    uint8_t* blob, moe_slice_index_entry_t* index, void* stream);
+/* Inverse: validates the index on the device (status word *bad = 1 on a
+ * non-contiguous or non-covering index) and scatters the slices out. */
+moe_status_t moe_split_blob_device(uint64_t blob_len, const uint8_t* blob, uint64_t n,
+                                   const moe_slice_index_entry_t* index, uint8_t* const* out,
+                                   int32_t* bad, void* stream);
+
+/* Routing (DESIGN.md Appendix A; K2): fp32 logits [T,E] ->
+ * expert/gate/position/keep [T,k], count1/count2/kept [E], aux (1 float).
+ * Bit-exact integers vs the oracle given identical logits. */
+typedef struct moe_routing_out {
+  int32_t* expert;   /* [T,k] */
+  float* gate;       /* [T,k] */
+  int32_t* position; /* [T,k] */
+  uint8_t* keep;     /* [T,k] */
+  int32_t* count1;   /* [E] pre-drop top-1 counts */
+  int32_t* count2;   /* [E] pre-drop top-2 counts */
+  int32_t* kept;     /* [E] min(count1+count2, C) */
+  float* aux_loss;   /* [1] */
+} moe_routing_out_t;
+
+moe_status_t moe_route(uint64_t tokens, uint32_t experts, uint32_t top_k, uint64_t capacity,
+                       const float* logits, const moe_routing_out_t* out, void* stream);
+
+/* Grouped GEMM (K5) exposed for tests and callers with their own layouts.
+ * bf16 inputs on tcgen05 (sm_100a), fp32 inputs on the SIMT FP32 path.
+ *   kind RAGGED_M : for group g, rows m < m[g]:
+ *       C[c_row[g]+m, n] = epi( sum_k A[a_row[g]+m, k] * B_{b[g]}(n, k) )
+ *     A row-major [*, K]; B_b = w + b*N*K, K-major ([N][K]) or MN-major ([K][N]).
+ *   kind RAGGED_K : for output o (= b[g]), C_o[m, n] += sum over groups g with
+ *     b[g] == o of sum_{r < m[g]} A[a_row[g]+r, m] * B[a_row[g]+r, n]
+ *     (A row-major [*, M], B row-major [*, N]; rows past m[g] up to the next
+ *     multiple of 64 must be zero).  Groups of one output must be contiguous.
+ * Group tables are device int32 arrays of length `groups`. */
+typedef enum moe_gemm_kind { MOE_GEMM_RAGGED_M = 0, MOE_GEMM_RAGGED_K = 1 } moe_gemm_kind_t;
+typedef enum moe_gemm_epilogue {
+  MOE_EPI_STORE = 0,      /* C = acc (+bias) in dtype_c                       */
+  MOE_EPI_GELU = 1,       /* C = act(acc+bias), C2 = acc+bias (pre-activation) */
+  MOE_EPI_DGELU = 2,      /* C = acc * gelu'(AUX[row, n])                      */
+  MOE_EPI_ATOMIC_ADD = 3  /* fp32 C += acc (split-K); transpose_c allowed       */
+} moe_gemm_epilogue_t;
+
+typedef struct moe_gemm_problem {
+  moe_gemm_kind_t kind;
+  moe_gemm_epilogue_t epilogue;
+  moe_dtype_t dtype_ab;   /* BF16 (tcgen05) or F32 (SIMT) */
+  moe_dtype_t dtype_c;    /* output dtype (F32 required for ATOMIC_ADD) */
+  int b_mn_major;         /* RAGGED_M: B stored [K][N] instead of [N][K] */
+  int transpose_c;        /* store C^T (C[n*ldc + m]) */
+  uint32_t groups;
+  uint32_t M, N, K;       /* RAGGED_M: N, K (M ragged). RAGGED_K: M, N (K ragged) */
+  uint64_t a_rows;        /* rows allocated in A (and B for RAGGED_K) */
+  uint32_t num_b;         /* number of B matrices (RAGGED_M) / outputs (RAGGED_K) */
+  const int32_t* m;       /* [groups] */
+  const int32_t* a_row;   /* [groups] */
+  const int32_t* c_row;   /* [groups] RAGGED_M only */
+  const int32_t* b;       /* [groups] */
+  const void* A;
+  const void* B;
+  void* C;
+  void* C2;               /* GELU pre-activation output (same layout as C) */
+  const void* aux;        /* DGELU: pre-activation, same layout/dtype as C */
+  const float* bias;      /* [num_b][N] or NULL */
+  uint64_t ldc;           /* elements; RAGGED_K outputs are [num_b][M][ldc] */
+  uint64_t lda;           /* A row stride in elements (0: K for RAGGED_M, M for RAGGED_K) */
+  uint64_t ldb;           /* B row stride in elements (0: natural) */
+  uint64_t b_rows;        /* rows allocated in B (0: num_b * (N or K), RAGGED_K: a_rows) */
+} moe_gemm_problem_t;
+
+moe_status_t moe_grouped_gemm(const moe_gemm_problem_t* problem, void* stream);
+
+/* ======================================================================
+ * 3. the MoE layer (K1..K6 + EP exchange), forward and backward
+ * ====================================================================== */
+
+typedef struct moe_layer_desc {
+  uint32_t num_experts;    /* E, global */
+  uint32_t top_k;          /* 1 (Switch) or 2 (GShard) */
+  uint32_t d_model;        /* d */
+  uint32_t d_ff;           /* d_ff */
+  double capacity_factor;  /* cf; C = ceil(k * cf * T / E) */
+  uint64_t tokens;         /* T, tokens per rank per call */
+  moe_dtype_t dtype;       /* BF16 (tcgen05 path) or F32 (SIMT FP32 path) */
+  int has_gate_bias;
+  uint32_t ep_size;        /* P ranks; E % P == 0 */
+  uint32_t ep_rank;
+  void* nccl_comm;         /* ncclComm_t when ep_size > 1 (see moe_comm_*) */
+} moe_layer_desc_t;
+
+typedef struct moe_layer* moe_layer_t;
+
+/* Parameters (device, caller-owned).  wg [E][d], bg [E] (fp32, optional);
+ * this rank's local experts (E/P of them): w1 [E/P][d_ff][d], b1 [E/P][d_ff]
+ * (fp32), w2 [E/P][d][d_ff], b2 [E/P][d] (fp32).  wg/w1/w2 in the layer dtype. */
+typedef struct moe_layer_params {
+  const void* wg;
+  const float* bg;
+  const void* w1;
+  const float* b1;
+  const void* w2;
+  const float* b2;
+} moe_layer_params_t;
+
+/* Gradients (device, fp32, overwritten): shapes as the parameters. */
+typedef struct moe_layer_grads {
+  float* dwg;
+  float* dbg;
+  float* dw1;
+  float* db1;
+  float* dw2;
+  float* db2;
+} moe_layer_grads_t;
+
+moe_status_t moe_layer_create(const moe_layer_desc_t* desc, moe_layer_t* out);
+moe_status_t moe_layer_destroy(moe_layer_t layer);
+/* C = ceil(k * cf * T / E) for this layer. */
+uint64_t moe_layer_capacity(moe_layer_t layer);
+
+/* y [T,d] = MoE(x [T,d]).  When logits_override != NULL routing uses those
+ * fp32 logits [T,E] instead of x wg^T + bg (parity tests). `routing` (optional)
+ * receives device copies of the routing outputs.  Saves what backward needs. */
+moe_status_t moe_layer_forward(moe_layer_t layer, const moe_layer_params_t* params, const void* x,
+                               void* y, const float* logits_override, float* logits_out,
+                               const moe_routing_out_t* routing, void* stream);
+
+/* Backward of the last forward: dy [T,d] and d_aux (upstream gradient of the
+ * aux loss) -> dx [T,d] and parameter gradients.  With ep_size > 1 dwg/dbg are
+ * summed over the EP group (the gate is replicated). */
+moe_status_t moe_layer_backward(moe_layer_t layer, const moe_layer_params_t* params, const void* dy,
+                                float d_aux, void* dx, const moe_layer_grads_t* grads,
+                                void* stream);
+
+/* One training step of the layer from HOST buffers (the end-to-end API):
+ * H2D x_host, dy_host (pinned) -> forward + backward -> D2H y_host, dx_host.
+ * Parameter gradients stay on the device in `grads`.  Enqueued on `stream`. */
+moe_status_t moe_layer_train_step_host(moe_layer_t layer, const moe_layer_params_t* params,
+                                       const void* x_host, const void* dy_host, float d_aux,
+                                       void* y_host, void* dx_host, const moe_layer_grads_t* grads,
+                                       void* stream);
+
+/* Per-phase device timings (ms) of the last forward/backward when profiling is
+ * enabled with moe_layer_set_profiling(layer, 1): names/values as parallel
+ * arrays; returns the count (<= capacity).  Synchronises the layer's events. */
+moe_status_t moe_layer_set_profiling(moe_layer_t layer, int enabled);
+moe_status_t moe_layer_phase_times(moe_layer_t layer, const char** names, float* ms,
+                                   uint32_t capacity, uint32_t* count);
+
+/* ----------------------------------------------------------------------
+ * EP communicator (NCCL over NVLink): the unique id is exchanged by the host
+ * (e.g. torch.distributed) as 128 opaque bytes.
+ * ---------------------------------------------------------------------- */
+moe_status_t moe_comm_unique_id(uint8_t id[128]);
+moe_status_t moe_comm_create(const uint8_t id[128], uint32_t nranks, uint32_t rank, void** comm);
+moe_status_t moe_comm_destroy(void* comm);
+
+/* Packed EP all-to-all (Fusion communication, §4.2): send holds one
+ * contiguous message of `bytes_per_peer` per destination rank in rank order;
+ * recv receives one per source rank in rank order (SPEC.md:336 receive order).
+ * fused = 0 issues `slices_per_peer` messages per peer instead (the unfused
+ * lowering of lower_slice_transfer, collectives.cpp:250-267) for comparison. */
+moe_status_t moe_alltoall_packed(void* comm, const void* send, void* recv, uint64_t bytes_per_peer,
+                                 uint32_t slices_per_peer, int fused, void* stream);
+
+/* ======================================================================
+ * 4. ring-of-sections inference (K7)
+ * ====================================================================== */
+
+/* N MoE layers whose expert weights live in pinned host memory rotate
+ * through K HBM slots (ring_offload.hpp:16-64).  Layer i's experts (w1,b1,w2,b2
+ * for all E experts of one rank, packed) are host_sections[i] of
+ * section_bytes; dense parameters (the gates) stay resident. */
+typedef struct moe_ring_desc {
+  uint32_t num_layers;
+  uint32_t ring_slots;
+  const void* const* host_sections; /* [num_layers] pinned host pointers */
+  const void* const* gate_weights;  /* [num_layers] device pointers (wg) */
+  const float* const* gate_bias;    /* [num_layers] device pointers or NULL */
+} moe_ring_desc_t;
+
+typedef struct moe_ring* moe_ring_t;
+
+typedef struct moe_ring_timeline {
+  /* per layer, ms since the start event */
+  float* load_start;
+  float* load_end;
+  float* compute_start;
+  float* compute_end;
+  float makespan_ms;
+  float compute_total_ms;
+  uint64_t peak_gpu_bytes;     /* dense + K * section */
+  uint64_t baseline_gpu_bytes; /* dense + N * section */
+  uint32_t slots;
+  int clamped;
+} moe_ring_timeline_t;
+
+moe_status_t moe_ring_create(moe_layer_t layer, const moe_ring_desc_t* desc, moe_ring_t* out);
+moe_status_t moe_ring_destroy(moe_ring_t ring);
+uint64_t moe_ring_section_bytes(moe_layer_t layer);
+/* Pack one layer's experts (device tensors) into a host section layout. */
+moe_status_t moe_ring_pack_section(moe_layer_t layer, const void* w1, const float* b1,
+                                   const void* w2, const float* b2, void* host_section);
+/* Residual stack h_{i+1} = h_i + MoE_i(h_i) over the N layers, expert weights
+ * streamed host -> HBM on a copy stream in the calculation-release-load order
+ * of build_schedule.  Fills `timeline` (synchronises on completion). */
+moe_status_t moe_ring_run(moe_ring_t ring, const void* x, void* y, moe_ring_timeline_t* timeline,
+                          void* stream);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* MOE_B200_H_ */

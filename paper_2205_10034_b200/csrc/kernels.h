@@ -1,0 +1,84 @@
+// Internal kernel entry points (host launchers) shared by the library's
+// translation units.  Not part of the public ABI (include/moe_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "moe_b200.h"
+
+namespace moe {
+
+// Kernel launch accounting (moe_kernel_launch_count).
+void count_launch(uint64_t n = 1);
+
+// K5: grouped GEMM. bf16 -> tcgen05 (gemm_tc.cu), fp32 -> SIMT FFMA (gemm_simt.cu).
+void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st);
+void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st);
+inline void grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
+  if (p.dtype_ab == MOE_DTYPE_BF16) tc_grouped_gemm(p, st);
+  else simt_grouped_gemm(p, st);
+}
+
+// K2: routing over fp32 logits (routing.cu).
+struct RouteWorkspace {
+  int32_t* chunk_cnt = nullptr;  // [2][nchunks][E]
+  int32_t* chunk_off = nullptr;  // [2][nchunks][E]
+  float* psum_part = nullptr;    // [nchunks][E]
+  int32_t* rank_local = nullptr; // [T][k]
+  uint64_t nchunks = 0;
+};
+uint64_t route_chunks(uint64_t T);
+void route_forward(uint64_t T, uint32_t E, uint32_t k, uint64_t C, const float* logits,
+                   const moe_routing_out_t& out, const RouteWorkspace& ws, cudaStream_t st);
+
+// Routing backward: dlogits [T, ld] (fp32 and/or bf16 copy) from dgate [T,k]
+// and d_aux.  Columns E..ld-1 of the bf16 copy are zeroed.
+void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, const int32_t* expert,
+                    const float* gate, const uint8_t* keep, const int32_t* count1,
+                    const float* dgate, float d_aux, float* dlogits_f32, void* dlogits_lp,
+                    moe_dtype_t lp_dtype, uint32_t ld, float* dbg, cudaStream_t st);
+
+// K3: dispatch tokens into the slot buffer [E][C][d] (send layout: rank-major,
+// then local expert, then position).  slot[t*k+i] = e*C+pos or -1.
+// Rows [kept_e, round_up(kept_e, pad)) of every expert are zero-filled.
+void dispatch_tokens(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C, uint32_t pad,
+                     moe_dtype_t dt, const void* x, const int32_t* expert, const int32_t* position,
+                     const int32_t* kept, void* buf, int32_t* slot, cudaStream_t st);
+
+// K6: combine y[t] = sum_i keep_i g_i Y[slot_i] (fp32 accumulate).
+void combine_tokens(uint64_t T, uint32_t d, uint32_t k, moe_dtype_t dt, const void* Y,
+                    const int32_t* slot, const float* gate, void* y, cudaStream_t st);
+
+// K6 backward: dgate[t,i] = <dy_t, Y[slot_i]>, dY[slot_i] = g_i * dy_t; pad rows
+// of dY zero-filled like dispatch.
+void combine_backward(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C, uint32_t pad,
+                      moe_dtype_t dt, const void* dy, const void* Y, const int32_t* slot,
+                      const float* gate, const int32_t* kept, void* dY, float* dgate,
+                      cudaStream_t st);
+
+// dx[t] = dx_gate[t] (fp32, may be null) + sum_i dXe[slot_i].
+void gather_dx(uint64_t T, uint32_t d, uint32_t k, moe_dtype_t dt, const void* dXe,
+               const int32_t* slot, const float* dx_gate, void* dx, cudaStream_t st);
+
+// Column sums over the valid rows of each (source, expert) slot group:
+// out[b][n] = sum over groups g with gb[g]==b of sum_{r<m[g]} X[a_row[g]+r][n].
+void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const int32_t* gb,
+                  uint32_t num_b, uint32_t N, moe_dtype_t dt, const void* X, float* out,
+                  cudaStream_t st, uint64_t max_rows);
+
+// Build the expert GEMM group tables for P source ranks x El local experts from
+// the received kept counts cnt[s][j]: group g = s*El + j, m = cnt, a_row =
+// (s*El+j)*Cs (Cs = slot stride), b = j.  Also the RAGGED_K order (grouped by
+// expert): gk = j*P + s with the same rows.
+void build_groups(uint32_t P, uint32_t El, uint64_t Cs, const int32_t* cnt, int32_t* gm,
+                  int32_t* ga, int32_t* gb, int32_t* gm_k, int32_t* ga_k, int32_t* gb_k,
+                  cudaStream_t st);
+
+// Data-plane helpers (moesim_ops.cu).
+void fill_uniform(void* out, uint64_t n, moe_dtype_t dt, uint64_t seed, double lo, double hi,
+                  cudaStream_t st);
+void convert_f32_to(const float* in, void* out, uint64_t n, moe_dtype_t dt, cudaStream_t st);
+
+}  // namespace moe

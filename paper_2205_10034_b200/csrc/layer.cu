@@ -1,0 +1,514 @@
+// The MoE layer: gate GEMM (K1) -> routing (K2) -> dispatch into the
+// Fusion-packed send buffer (K3) -> EP all-to-all over NCCL (K4) -> grouped
+// expert FFN on tcgen05 (K5) -> all-to-all back (K4) -> weighted combine (K6),
+// and the backward of all of it (4 all-to-alls per layer).
+//
+// Layout in HBM:
+//   send/home buffers  [E][Cs][d]       expert-major; experts of rank r are the
+//                                       contiguous block r*El..r*El+El-1, so the
+//                                       message to rank r is ONE contiguous
+//                                       region (Fusion packing, collectives.cpp:
+//                                       88-98: SliceIndex = (j, j*Cs*d, kept*d))
+//   recv buffers       [P][El][Cs][d]   per (source rank, local expert) slice,
+//                                       receive order = source rank order
+//                                       (alltoall_flat, collectives.cpp:10-21)
+//   expert activations [P*El*Cs][d_ff]  same row space as recv
+// Cs = C rounded up to 64 rows; rows [kept, round_up(kept,64)) are zero so the
+// weight-gradient GEMM can run whole 64-row K blocks.  No host synchronisation:
+// every count lives on the device and the GEMM tile schedulers read it there.
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "layer.h"
+
+namespace moe {
+
+#define MOE_NCCL(expr)                                                                  \
+  do {                                                                                  \
+    ncclResult_t _r = (expr);                                                           \
+    if (_r != ncclSuccess)                                                              \
+      ::moe::fail(MOE_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));    \
+  } while (0)
+
+namespace {
+
+template <typename T>
+T* dalloc(std::vector<void*>& owned, uint64_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  MOE_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+void* dalloc_bytes(std::vector<void*>& owned, uint64_t n) {
+  void* p = nullptr;
+  MOE_CUDA(cudaMalloc(&p, n ? n : 16));
+  owned.push_back(p);
+  return p;
+}
+
+}  // namespace
+
+Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
+  E = d.num_experts;
+  k = d.top_k;
+  dm = d.d_model;
+  dff = d.d_ff;
+  T = d.tokens;
+  P = d.ep_size ? d.ep_size : 1;
+  rank = d.ep_rank;
+  dt = d.dtype;
+  config_check(E >= 1, "layer.num_experts: must be >= 1");
+  config_check(E <= 256, "layer.num_experts: must be <= 256");
+  config_check(k == 1 || k == 2, "layer.top_k: must be 1 or 2");
+  config_check(k == 1 || E >= 2, "layer.top_k: top-2 needs >= 2 experts");
+  config_check(d.capacity_factor > 0.0, "layer.capacity_factor: must be > 0");
+  config_check(dt == MOE_DTYPE_BF16 || dt == MOE_DTYPE_F32, "layer.dtype: must be bf16 or fp32");
+  config_check(E % P == 0, "layer.ep_size: must divide num_experts");
+  config_check(rank < P, "layer.ep_rank: must be < ep_size");
+  config_check(P == 1 || d.nccl_comm != nullptr, "layer.nccl_comm: required when ep_size > 1");
+  if (dt == MOE_DTYPE_BF16) {
+    config_check(dm % 128 == 0, "layer.d_model: bf16 path needs a multiple of 128");
+    config_check(dff % 128 == 0, "layer.d_ff: bf16 path needs a multiple of 128");
+  } else {
+    config_check(dm % 8 == 0, "layer.d_model: must be a multiple of 8");
+    config_check(dff % 8 == 0, "layer.d_ff: must be a multiple of 8");
+  }
+  El = E / P;
+  esz = dt == MOE_DTYPE_BF16 ? 2 : 4;
+  comm = d.nccl_comm;
+  const double c = (double)k * d.capacity_factor * (double)T / (double)E;
+  C = (uint64_t)std::ceil(c);
+  pad = dt == MOE_DTYPE_BF16 ? 64 : 1;
+  Cs = round_up(C ? C : 1, pad);
+  rows = (uint64_t)P * El * Cs;
+  Epad = (uint32_t)round_up(E, 64);
+  config_check(rows < (1ull << 31), "layer.tokens: slot rows exceed int32 indexing");
+
+  MOE_CUDA(cudaGetDevice(&device));
+  // routing state
+  logits = dalloc<float>(owned, T * E);
+  expert = dalloc<int32_t>(owned, T * k);
+  position = dalloc<int32_t>(owned, T * k);
+  slot = dalloc<int32_t>(owned, T * k);
+  gate = dalloc<float>(owned, T * k);
+  keep = dalloc<uint8_t>(owned, T * k);
+  count1 = dalloc<int32_t>(owned, E);
+  count2 = dalloc<int32_t>(owned, E);
+  kept = dalloc<int32_t>(owned, E);
+  aux = dalloc<float>(owned, 1);
+  rws.nchunks = route_chunks(T);
+  rws.chunk_cnt = dalloc<int32_t>(owned, 2 * rws.nchunks * E);
+  rws.chunk_off = dalloc<int32_t>(owned, 2 * rws.nchunks * E);
+  rws.psum_part = dalloc<float>(owned, rws.nchunks * E);
+  rws.rank_local = dalloc<int32_t>(owned, T * k);
+  // token buffers
+  const uint64_t slot_bytes = (uint64_t)E * Cs * dm * esz;
+  xs = dalloc_bytes(owned, slot_bytes);
+  xr = P > 1 ? dalloc_bytes(owned, slot_bytes) : xs;
+  cnt_recv = P > 1 ? dalloc<int32_t>(owned, E) : kept;
+  gm = dalloc<int32_t>(owned, E);
+  ga = dalloc<int32_t>(owned, E);
+  gb = dalloc<int32_t>(owned, E);
+  gmk = dalloc<int32_t>(owned, E);
+  gak = dalloc<int32_t>(owned, E);
+  gbk = dalloc<int32_t>(owned, E);
+  H = dalloc_bytes(owned, rows * dff * esz);
+  Aact = dalloc_bytes(owned, rows * dff * esz);
+  Yl = dalloc_bytes(owned, slot_bytes);
+  Yh = P > 1 ? dalloc_bytes(owned, slot_bytes) : Yl;
+  // backward
+  dgate = dalloc<float>(owned, T * k);
+  dYs = dalloc_bytes(owned, slot_bytes);
+  dYr = P > 1 ? dalloc_bytes(owned, slot_bytes) : dYs;
+  dH = dalloc_bytes(owned, rows * dff * esz);
+  dXl = dalloc_bytes(owned, slot_bytes);
+  dXh = P > 1 ? dalloc_bytes(owned, slot_bytes) : dXl;
+  if (dt == MOE_DTYPE_BF16) dl_lp = dalloc_bytes(owned, T * Epad * 2);
+  else dl_f32 = dalloc<float>(owned, T * E);
+  dxg = dalloc<float>(owned, T * dm);
+  // Every row of the activation buffers holds finite values from here on, so
+  // zero pad rows of the partner operand annihilate them in the RAGGED_K GEMMs.
+  MOE_CUDA(cudaMemset(xs, 0, slot_bytes));
+  if (xr != xs) MOE_CUDA(cudaMemset(xr, 0, slot_bytes));
+  MOE_CUDA(cudaMemset(H, 0, rows * dff * esz));
+  MOE_CUDA(cudaMemset(Aact, 0, rows * dff * esz));
+  MOE_CUDA(cudaMemset(dH, 0, rows * dff * esz));
+  MOE_CUDA(cudaMemset(dYs, 0, slot_bytes));
+  if (dYr != dYs) MOE_CUDA(cudaMemset(dYr, 0, slot_bytes));
+  // gate GEMM tables: one group of T rows; split-K groups for dwg
+  {
+    std::vector<int32_t> one = {(int32_t)T, 0, 0, 0};
+    gate_tab = dalloc<int32_t>(owned, 4);
+    MOE_CUDA(cudaMemcpy(gate_tab, one.data(), 16, cudaMemcpyHostToDevice));
+    const uint64_t split_rows = 1024;
+    nsplit = (uint32_t)std::max<uint64_t>(1, ceil_div(T, split_rows));
+    config_check(nsplit <= 1024, "layer.tokens: too many tokens for the split-K gate GEMM");
+    std::vector<int32_t> sm(nsplit), sa(nsplit), sb(nsplit, 0);
+    for (uint32_t s = 0; s < nsplit; ++s) {
+      sa[s] = (int32_t)(s * split_rows);
+      sm[s] = (int32_t)std::min<uint64_t>(split_rows, T - std::min<uint64_t>(T, s * split_rows));
+    }
+    split_m = dalloc<int32_t>(owned, nsplit);
+    split_a = dalloc<int32_t>(owned, nsplit);
+    split_b = dalloc<int32_t>(owned, nsplit);
+    MOE_CUDA(cudaMemcpy(split_m, sm.data(), nsplit * 4, cudaMemcpyHostToDevice));
+    MOE_CUDA(cudaMemcpy(split_a, sa.data(), nsplit * 4, cudaMemcpyHostToDevice));
+    MOE_CUDA(cudaMemcpy(split_b, sb.data(), nsplit * 4, cudaMemcpyHostToDevice));
+  }
+  for (int i = 0; i < kMaxPhases + 1; ++i) MOE_CUDA(cudaEventCreate(&ev[i]));
+}
+
+Layer::~Layer() {
+  for (int i = 0; i < kMaxPhases + 1; ++i) cudaEventDestroy(ev[i]);
+  for (void* p : owned) cudaFree(p);
+  if (x_stage) cudaFree(x_stage);
+}
+
+void Layer::mark(const char* name, cudaStream_t st) {
+  if (!profiling || nphase >= kMaxPhases) return;
+  phase_name[nphase] = name;
+  MOE_CUDA(cudaEventRecord(ev[nphase + 1], st));
+  ++nphase;
+}
+
+void Layer::a2a(const void* send, void* recv, uint64_t bytes_per_peer, cudaStream_t st) {
+  MOE_NCCL(ncclAlltoAll(send, recv, bytes_per_peer, ncclUint8, (ncclComm_t)comm, st));
+}
+
+moe_gemm_problem_t Layer::expert_problem() const {
+  moe_gemm_problem_t p;
+  std::memset(&p, 0, sizeof(p));
+  p.kind = MOE_GEMM_RAGGED_M;
+  p.dtype_ab = dt;
+  p.dtype_c = dt;
+  p.groups = P * El;
+  p.a_rows = rows;
+  p.num_b = El;
+  p.m = gm;
+  p.a_row = ga;
+  p.c_row = ga;
+  p.b = gb;
+  return p;
+}
+
+void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const float* override_logits,
+                    float* logits_out, const moe_routing_out_t* rout, cudaStream_t st) {
+  arg_check(x != nullptr && y != nullptr, "forward.x/y: must be non-null");
+  arg_check(w.w1 && w.w2 && w.b1 && w.b2, "forward.params: expert weights must be non-null");
+  arg_check(override_logits || w.wg, "forward.params.wg: gate weight required");
+  nphase = 0;
+  x_saved_ptr = x;
+  if (profiling) MOE_CUDA(cudaEventRecord(ev[0], st));
+  // K1: logits = x wg^T (+ bg), fp32 out
+  if (override_logits) {
+    MOE_CUDA(cudaMemcpyAsync(logits, override_logits, T * E * 4, cudaMemcpyDeviceToDevice, st));
+  } else if (T) {
+    moe_gemm_problem_t p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = MOE_GEMM_RAGGED_M;
+    p.epilogue = MOE_EPI_STORE;
+    p.dtype_ab = dt;
+    p.dtype_c = MOE_DTYPE_F32;
+    p.groups = 1;
+    p.N = E;
+    p.K = dm;
+    p.a_rows = T;
+    p.num_b = 1;
+    p.m = gate_tab;
+    p.a_row = gate_tab + 1;
+    p.c_row = gate_tab + 2;
+    p.b = gate_tab + 3;
+    p.A = x;
+    p.B = w.wg;
+    p.C = logits;
+    p.bias = desc.has_gate_bias ? w.bg : nullptr;
+    p.ldc = E;
+    grouped_gemm(p, st);
+  }
+  mark("gate_gemm", st);
+  // K2: routing
+  moe_routing_out_t ro{expert, gate, position, keep, count1, count2, kept, aux};
+  route_forward(T, E, k, C, logits, ro, rws, st);
+  mark("route", st);
+  // K3: dispatch into the Fusion-packed send buffer
+  dispatch_tokens(T, dm, E, k, C, pad, dt, x, expert, position, kept, xs, slot, st);
+  mark("dispatch", st);
+  // K4: counts + payload exchange (one message per peer)
+  if (P > 1) {
+    MOE_NCCL(ncclGroupStart());
+    a2a(kept, cnt_recv, El * sizeof(int32_t), st);
+    a2a(xs, xr, El * Cs * dm * esz, st);
+    MOE_NCCL(ncclGroupEnd());
+  }
+  mark("a2a_dispatch", st);
+  build_groups(P, El, Cs, cnt_recv, gm, ga, gb, gmk, gak, gbk, st);
+  // K5: H = X W1^T + b1 (stored), A = gelu(H); Y = A W2^T + b2
+  {
+    moe_gemm_problem_t p = expert_problem();
+    p.epilogue = MOE_EPI_GELU;
+    p.N = dff;
+    p.K = dm;
+    p.A = xr;
+    p.B = w.w1;
+    p.C = Aact;
+    p.C2 = H;
+    p.bias = w.b1;
+    p.ldc = dff;
+    grouped_gemm(p, st);
+  }
+  mark("ffn1", st);
+  {
+    moe_gemm_problem_t p = expert_problem();
+    p.epilogue = MOE_EPI_STORE;
+    p.N = dm;
+    p.K = dff;
+    p.A = Aact;
+    p.B = w.w2;
+    p.C = Yl;
+    p.bias = w.b2;
+    p.ldc = dm;
+    grouped_gemm(p, st);
+  }
+  mark("ffn2", st);
+  if (P > 1) a2a(Yl, Yh, El * Cs * dm * esz, st);
+  mark("a2a_combine", st);
+  // K6: weighted combine
+  combine_tokens(T, dm, k, dt, Yh, slot, gate, y, st);
+  mark("combine", st);
+  if (logits_out)
+    MOE_CUDA(cudaMemcpyAsync(logits_out, logits, T * E * 4, cudaMemcpyDeviceToDevice, st));
+  if (rout) {
+    auto cp = [&](void* dst, const void* src, uint64_t n) {
+      if (dst) MOE_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, st));
+    };
+    cp(rout->expert, expert, T * k * 4);
+    cp(rout->gate, gate, T * k * 4);
+    cp(rout->position, position, T * k * 4);
+    cp(rout->keep, keep, T * k);
+    cp(rout->count1, count1, E * 4);
+    cp(rout->count2, count2, E * 4);
+    cp(rout->kept, kept, E * 4);
+    cp(rout->aux_loss, aux, 4);
+  }
+  has_forward = true;
+}
+
+void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, void* dx,
+                     const moe_layer_grads_t& g, cudaStream_t st) {
+  require(has_forward, MOE_ERR_LOGIC, "backward: no forward pass recorded on this layer");
+  arg_check(dy != nullptr && dx != nullptr, "backward.dy/dx: must be non-null");
+  arg_check(g.dw1 && g.db1 && g.dw2 && g.db2 && g.dwg, "backward.grads: must be non-null");
+  arg_check(w.wg != nullptr, "backward.params.wg: gate weight required");
+  nphase = 0;
+  if (profiling) MOE_CUDA(cudaEventRecord(ev[0], st));
+  // K6^T: dgate and the gate-scaled dY into the send layout (+ zero pad rows)
+  combine_backward(T, dm, E, k, C, pad, dt, dy, Yh, slot, gate, kept, dYs, dgate, st);
+  mark("combine_bwd", st);
+  // K2^T: dlogits
+  if (desc.has_gate_bias && g.dbg) MOE_CUDA(cudaMemsetAsync(g.dbg, 0, E * 4, st));
+  route_backward(T, E, k, logits, expert, gate, keep, count1, dgate, d_aux, dl_f32, dl_lp,
+                 dt == MOE_DTYPE_BF16 ? MOE_DTYPE_BF16 : MOE_DTYPE_F32,
+                 dt == MOE_DTYPE_BF16 ? Epad : E, desc.has_gate_bias ? g.dbg : nullptr, st);
+  mark("route_bwd", st);
+  if (P > 1) a2a(dYs, dYr, El * Cs * dm * esz, st);
+  mark("a2a_dy", st);
+  // K5^T dgrad: dH = (dY W2) * gelu'(H); dXe = dH W1
+  {
+    moe_gemm_problem_t p = expert_problem();
+    p.epilogue = MOE_EPI_DGELU;
+    p.b_mn_major = 1;
+    p.N = dff;
+    p.K = dm;
+    p.A = dYr;
+    p.B = w.w2;
+    p.C = dH;
+    p.aux = H;
+    p.ldc = dff;
+    grouped_gemm(p, st);
+  }
+  mark("dgrad_ffn2", st);
+  {
+    moe_gemm_problem_t p = expert_problem();
+    p.epilogue = MOE_EPI_STORE;
+    p.b_mn_major = 1;
+    p.N = dm;
+    p.K = dff;
+    p.A = dH;
+    p.B = w.w1;
+    p.C = dXl;
+    p.ldc = dm;
+    grouped_gemm(p, st);
+  }
+  mark("dgrad_ffn1", st);
+  if (P > 1) a2a(dXl, dXh, El * Cs * dm * esz, st);
+  mark("a2a_dx", st);
+  // K5^T wgrad: dW1[j] = sum dH^T X, dW2[j] = sum dY^T A (RAGGED_K over slices)
+  {
+    moe_gemm_problem_t p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = MOE_GEMM_RAGGED_K;
+    p.epilogue = MOE_EPI_STORE;
+    p.dtype_ab = dt;
+    p.dtype_c = MOE_DTYPE_F32;
+    p.groups = P * El;
+    p.a_rows = rows;
+    p.num_b = El;
+    p.m = gmk;
+    p.a_row = gak;
+    p.b = gbk;
+    p.M = dff;
+    p.N = dm;
+    p.A = dH;
+    p.B = xr;
+    p.C = g.dw1;
+    p.ldc = dm;
+    grouped_gemm(p, st);
+    mark("wgrad_w1", st);
+    p.M = dm;
+    p.N = dff;
+    p.A = dYr;
+    p.B = Aact;
+    p.C = g.dw2;
+    p.ldc = dff;
+    grouped_gemm(p, st);
+    mark("wgrad_w2", st);
+  }
+  group_colsum(P * El, gm, ga, gb, El, dff, dt, dH, g.db1, st, Cs);
+  group_colsum(P * El, gm, ga, gb, El, dm, dt, dYr, g.db2, st, Cs);
+  mark("bias_grads", st);
+  // gate: dx_gate = dlogits wg ; dwg = dlogits^T x (split-K, fp32 atomics)
+  if (T) {
+    moe_gemm_problem_t p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = MOE_GEMM_RAGGED_M;
+    p.epilogue = MOE_EPI_STORE;
+    p.dtype_ab = dt;
+    p.dtype_c = MOE_DTYPE_F32;
+    p.b_mn_major = 1;
+    p.groups = 1;
+    p.N = dm;
+    p.K = dt == MOE_DTYPE_BF16 ? Epad : E;
+    p.a_rows = T;
+    p.num_b = 1;
+    p.b_rows = E;
+    p.m = gate_tab;
+    p.a_row = gate_tab + 1;
+    p.c_row = gate_tab + 2;
+    p.b = gate_tab + 3;
+    p.A = dt == MOE_DTYPE_BF16 ? dl_lp : (const void*)dl_f32;
+    p.B = w.wg;
+    p.C = dxg;
+    p.ldc = dm;
+    grouped_gemm(p, st);
+  }
+  mark("gate_dgrad", st);
+  MOE_CUDA(cudaMemsetAsync(g.dwg, 0, (uint64_t)E * dm * 4, st));
+  if (T) {
+    moe_gemm_problem_t p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = MOE_GEMM_RAGGED_K;
+    p.epilogue = MOE_EPI_ATOMIC_ADD;
+    p.dtype_ab = dt;
+    p.dtype_c = MOE_DTYPE_F32;
+    p.transpose_c = 1;
+    p.groups = nsplit;
+    p.M = dm;
+    p.N = E;
+    p.a_rows = T;
+    p.b_rows = T;
+    p.num_b = 1;
+    p.m = split_m;
+    p.a_row = split_a;
+    p.b = split_b;
+    p.A = x_saved_ptr;
+    p.B = dt == MOE_DTYPE_BF16 ? dl_lp : (const void*)dl_f32;
+    p.ldb = dt == MOE_DTYPE_BF16 ? Epad : E;
+    p.C = g.dwg;
+    p.ldc = dm;
+    grouped_gemm(p, st);
+  }
+  mark("gate_wgrad", st);
+  gather_dx(T, dm, k, dt, dXh, slot, dxg, dx, st);
+  mark("gather_dx", st);
+  if (P > 1) {
+    MOE_NCCL(ncclGroupStart());
+    MOE_NCCL(ncclAllReduce(g.dwg, g.dwg, (uint64_t)E * dm, ncclFloat32, ncclSum, (ncclComm_t)comm, st));
+    if (desc.has_gate_bias && g.dbg)
+      MOE_NCCL(ncclAllReduce(g.dbg, g.dbg, E, ncclFloat32, ncclSum, (ncclComm_t)comm, st));
+    MOE_NCCL(ncclGroupEnd());
+  }
+  mark("allreduce_gate", st);
+}
+
+void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, const void* dy_host,
+                            float d_aux, void* y_host, void* dx_host, const moe_layer_grads_t& g,
+                            cudaStream_t st) {
+  const uint64_t bytes = T * dm * esz;
+  if (!x_stage) {
+    MOE_CUDA(cudaMalloc(&x_stage, 4 * bytes + 64));
+  }
+  uint8_t* base = static_cast<uint8_t*>(x_stage);
+  void* xd = base;
+  void* dyd = base + bytes;
+  void* yd = base + 2 * bytes;
+  void* dxd = base + 3 * bytes;
+  MOE_CUDA(cudaMemcpyAsync(xd, x_host, bytes, cudaMemcpyHostToDevice, st));
+  MOE_CUDA(cudaMemcpyAsync(dyd, dy_host, bytes, cudaMemcpyHostToDevice, st));
+  x_saved_ptr = xd;
+  forward(w, xd, yd, nullptr, nullptr, nullptr, st);
+  backward(w, dyd, d_aux, dxd, g, st);
+  MOE_CUDA(cudaMemcpyAsync(y_host, yd, bytes, cudaMemcpyDeviceToHost, st));
+  MOE_CUDA(cudaMemcpyAsync(dx_host, dxd, bytes, cudaMemcpyDeviceToHost, st));
+}
+
+// --------------------------------------------------------------- comm -----
+void comm_unique_id(uint8_t id[128]) {
+  ncclUniqueId u;
+  MOE_NCCL(ncclGetUniqueId(&u));
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+}
+
+void* comm_create(const uint8_t id[128], uint32_t nranks, uint32_t rank) {
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclComm_t c = nullptr;
+  MOE_NCCL(ncclCommInitRank(&c, (int)nranks, u, (int)rank));
+  return c;
+}
+
+void comm_destroy(void* c) {
+  if (c) MOE_NCCL(ncclCommDestroy((ncclComm_t)c));
+}
+
+void alltoall_packed(void* comm, const void* send, void* recv, uint64_t bytes_per_peer,
+                     uint32_t slices_per_peer, int fused, cudaStream_t st) {
+  ncclComm_t c = (ncclComm_t)comm;
+  int n = 0, me = 0;
+  MOE_NCCL(ncclCommCount(c, &n));
+  MOE_NCCL(ncclCommUserRank(c, &me));
+  if (fused || slices_per_peer <= 1) {
+    MOE_NCCL(ncclAlltoAll(send, recv, bytes_per_peer, ncclUint8, c, st));
+    return;
+  }
+  arg_check(bytes_per_peer % slices_per_peer == 0,
+            "alltoall.slices_per_peer: must divide bytes_per_peer");
+  const uint64_t sl = bytes_per_peer / slices_per_peer;
+  MOE_NCCL(ncclGroupStart());
+  for (int p = 0; p < n; ++p) {
+    for (uint32_t s = 0; s < slices_per_peer; ++s) {
+      const uint64_t off = (uint64_t)p * bytes_per_peer + s * sl;
+      MOE_NCCL(ncclSend(static_cast<const uint8_t*>(send) + off, sl, ncclUint8, p, c, st));
+      MOE_NCCL(ncclRecv(static_cast<uint8_t*>(recv) + off, sl, ncclUint8, p, c, st));
+    }
+  }
+  MOE_NCCL(ncclGroupEnd());
+}
+
+}  // namespace moe

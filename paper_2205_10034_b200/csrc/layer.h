@@ -1,0 +1,100 @@
+// Internal MoE-layer object behind the opaque moe_layer_t handle.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "kernels.h"
+#include "moe_b200.h"
+
+namespace moe {
+
+struct Layer {
+  static constexpr int kMaxPhases = 32;
+
+  explicit Layer(const moe_layer_desc_t& d);
+  ~Layer();
+  Layer(const Layer&) = delete;
+  Layer& operator=(const Layer&) = delete;
+
+  void forward(const moe_layer_params_t& w, const void* x, void* y, const float* override_logits,
+               float* logits_out, const moe_routing_out_t* rout, cudaStream_t st);
+  void backward(const moe_layer_params_t& w, const void* dy, float d_aux, void* dx,
+                const moe_layer_grads_t& g, cudaStream_t st);
+  void train_step_host(const moe_layer_params_t& w, const void* x_host, const void* dy_host,
+                       float d_aux, void* y_host, void* dx_host, const moe_layer_grads_t& g,
+                       cudaStream_t st);
+
+  moe_gemm_problem_t expert_problem() const;
+  void a2a(const void* send, void* recv, uint64_t bytes_per_peer, cudaStream_t st);
+  void mark(const char* name, cudaStream_t st);
+
+  moe_layer_desc_t desc;
+  uint32_t E = 0, k = 0, dm = 0, dff = 0, P = 1, rank = 0, El = 0, Epad = 0;
+  uint64_t T = 0, C = 0, Cs = 0, rows = 0;
+  uint32_t pad = 1;
+  moe_dtype_t dt = MOE_DTYPE_BF16;
+  uint64_t esz = 2;
+  void* comm = nullptr;
+  int device = 0;
+
+  std::vector<void*> owned;
+  // routing state
+  float* logits = nullptr;
+  int32_t *expert = nullptr, *position = nullptr, *slot = nullptr;
+  float* gate = nullptr;
+  uint8_t* keep = nullptr;
+  int32_t *count1 = nullptr, *count2 = nullptr, *kept = nullptr;
+  float* aux = nullptr;
+  RouteWorkspace rws;
+  // token/expert buffers
+  void *xs = nullptr, *xr = nullptr;
+  int32_t* cnt_recv = nullptr;
+  int32_t *gm = nullptr, *ga = nullptr, *gb = nullptr, *gmk = nullptr, *gak = nullptr,
+          *gbk = nullptr;
+  void *H = nullptr, *Aact = nullptr, *Yl = nullptr, *Yh = nullptr;
+  // backward buffers
+  float* dgate = nullptr;
+  void *dYs = nullptr, *dYr = nullptr, *dH = nullptr, *dXl = nullptr, *dXh = nullptr;
+  float* dl_f32 = nullptr;
+  void* dl_lp = nullptr;
+  float* dxg = nullptr;
+  // gate GEMM tables
+  int32_t* gate_tab = nullptr;
+  int32_t *split_m = nullptr, *split_a = nullptr, *split_b = nullptr;
+  uint32_t nsplit = 1;
+  const void* x_saved_ptr = nullptr;
+  void* x_stage = nullptr;
+  bool has_forward = false;
+  // profiling
+  bool profiling = false;
+  int nphase = 0;
+  const char* phase_name[kMaxPhases] = {};
+  cudaEvent_t ev[kMaxPhases + 1] = {};
+};
+
+void comm_unique_id(uint8_t id[128]);
+void* comm_create(const uint8_t id[128], uint32_t nranks, uint32_t rank);
+void comm_destroy(void* c);
+void alltoall_packed(void* comm, const void* send, void* recv, uint64_t bytes_per_peer,
+                     uint32_t slices_per_peer, int fused, cudaStream_t st);
+
+// moesim_ops.cu
+void gen_trace_device(uint64_t seed, uint32_t steps, uint32_t ranks, uint32_t experts,
+                      uint64_t tokens, double skew, uint64_t* counts, cudaStream_t st);
+void imbalance_device(uint64_t rows, uint32_t experts, const uint64_t* counts,
+                      unsigned long long* out2, cudaStream_t st);
+void alltoall_flat_device(uint64_t R, const uint64_t* lens, const uint64_t* in_off,
+                          const uint8_t* in, const uint64_t* out_off, uint8_t* out,
+                          uint64_t max_len, cudaStream_t st);
+void fuse_slices_device(uint64_t n, const uint8_t* const* slices, const uint64_t* lens,
+                        uint8_t* blob, moe_slice_index_entry_t* index, uint64_t max_len,
+                        cudaStream_t st);
+void split_blob_device(uint64_t blob_len, const uint8_t* blob, uint64_t n,
+                       const moe_slice_index_entry_t* index, uint8_t* const* out, int32_t* bad,
+                       uint64_t max_len, cudaStream_t st);
+
+}  // namespace moe

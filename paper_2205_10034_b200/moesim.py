@@ -1,0 +1,163 @@
+"""Python mirror of the reference's moesim:: functions on the path.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/core/include/moesim/{collectives,workload,ring_offload}.hpp,
+executed by libmoe_b200.so on the GPU (host buffers in, host buffers out — the
+reference's value-semantics calling convention).  Chunks are ``bytes``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ._lib import ConfigError, SliceIndexEntry, call, lib  # noqa: F401
+
+Chunk = bytes
+
+
+@dataclass
+class ShardedPayload:
+    """collectives.hpp:19-33 — square R x R chunk matrix, row-major [src][dst]."""
+    ranks: int = 0
+    chunks: List[bytes] = field(default_factory=list)
+
+    @staticmethod
+    def make(ranks: int) -> "ShardedPayload":
+        return ShardedPayload(ranks, [b""] * (ranks * ranks))
+
+    def at(self, src: int, dst: int) -> bytes:
+        return self.chunks[src * self.ranks + dst]
+
+    def set(self, src: int, dst: int, chunk: bytes) -> None:
+        self.chunks[src * self.ranks + dst] = bytes(chunk)
+
+
+def _u64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.uint64))
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p) if a.size else None
+
+
+def alltoall_flat(payload: ShardedPayload) -> ShardedPayload:
+    """collectives.cpp:10-21: chunks'[i][j] = chunks[j][i]; non-square -> ValueError."""
+    n = len(payload.chunks)
+    lens = _u64([len(c) for c in payload.chunks])
+    data = np.frombuffer(b"".join(payload.chunks), dtype=np.uint8).copy()
+    out_lens = np.zeros(n, dtype=np.uint64)
+    out = np.zeros(max(int(lens.sum()), 1), dtype=np.uint8)
+    call("moesim_alltoall_flat", payload.ranks, n, _ptr(lens), _ptr(data), _ptr(out_lens),
+         _ptr(out))
+    res = ShardedPayload.make(payload.ranks)
+    o = 0
+    for i in range(n):
+        ln = int(out_lens[i])
+        res.chunks[i] = out[o:o + ln].tobytes()
+        o += ln
+    return res
+
+
+@dataclass
+class FusedBlob:
+    blob: bytes
+    index: List[tuple]  # (slice_id, offset, length)
+
+
+def fuse_slices(slices: Sequence[bytes]) -> FusedBlob:
+    """collectives.cpp:88-98; empty list -> ValueError."""
+    n = len(slices)
+    lens = _u64([len(s) for s in slices])
+    data = np.frombuffer(b"".join(slices), dtype=np.uint8).copy()
+    blob = np.zeros(max(int(lens.sum()) if n else 0, 1), dtype=np.uint8)
+    idx = (SliceIndexEntry * max(n, 1))()
+    call("moesim_fuse_slices", n, _ptr(lens) if n else None, _ptr(data), _ptr(blob),
+         C.cast(idx, C.c_void_p))
+    total = int(lens.sum()) if n else 0
+    return FusedBlob(blob[:total].tobytes(),
+                     [(idx[i].slice_id, idx[i].offset, idx[i].length) for i in range(n)])
+
+
+def split_blob(blob: bytes, index: Sequence[tuple]) -> List[bytes]:
+    """collectives.cpp:100-118; non-contiguous / non-covering index -> ValueError."""
+    n = len(index)
+    idx = (SliceIndexEntry * max(n, 1))()
+    for i, (sid, off, ln) in enumerate(index):
+        idx[i].slice_id, idx[i].offset, idx[i].length = sid, off, ln
+    b = np.frombuffer(bytes(blob), dtype=np.uint8).copy()
+    out = np.zeros(max(len(blob), 1), dtype=np.uint8)
+    call("moesim_split_blob", len(blob), _ptr(b), n, C.cast(idx, C.c_void_p), _ptr(out))
+    res, o = [], 0
+    for (_, _, ln) in index:
+        res.append(out[o:o + ln].tobytes())
+        o += ln
+    return res
+
+
+@dataclass
+class RoutingTrace:
+    """workload.hpp:14-30: counts[step][rank][expert] (uint64)."""
+    steps: int
+    ranks: int
+    experts: int
+    tokens_per_rank: int
+    counts: np.ndarray
+
+    def at(self, s: int, r: int, e: int) -> int:
+        return int(self.counts[s, r, e])
+
+    def expert_total(self, e: int) -> int:
+        return int(self.counts[:, :, e].sum())
+
+
+def gen_trace(seed: int, steps: int, ranks: int, experts: int, tokens_per_rank: int,
+              skew: float) -> RoutingTrace:
+    """workload.cpp:19-53 (device-generated, bit-identical)."""
+    counts = np.zeros((steps, ranks, max(experts, 1)), dtype=np.uint64)
+    call("moesim_gen_trace", seed, steps, ranks, experts, tokens_per_rank, float(skew),
+         counts.ctypes.data_as(C.c_void_p))
+    return RoutingTrace(steps, ranks, experts, tokens_per_rank, counts[:, :, :experts])
+
+
+def imbalance_ratio(trace: RoutingTrace) -> float:
+    """workload.cpp:55-66; zero tokens -> ConfigError."""
+    counts = np.ascontiguousarray(trace.counts, dtype=np.uint64)
+    out = C.c_double(0.0)
+    call("moesim_imbalance_ratio", trace.steps, trace.ranks, trace.experts,
+         counts.ctypes.data_as(C.c_void_p) if counts.size else None, C.byref(out))
+    return out.value
+
+
+LOAD, COMPUTE, RELEASE = 0, 1, 2
+
+
+@dataclass
+class RingOp:
+    kind: int
+    layer: int
+    slot: int
+    waits_release_of: Optional[int]
+
+
+@dataclass
+class RingSchedule:
+    ops: List[RingOp]
+    slots: int
+    clamped: bool
+
+
+def build_schedule(num_layers: int, ring_slots: int) -> RingSchedule:
+    """ring_offload.cpp:31-50; ring_slots == 0 or num_layers == 0 -> ConfigError."""
+    cap = 3 * max(num_layers, 1) + max(num_layers, 1)
+    ops = np.zeros((cap, 4), dtype=np.int64)
+    n = C.c_uint64(0)
+    slots = C.c_uint32(0)
+    clamped = C.c_int(0)
+    call("moesim_ring_build_schedule", num_layers, ring_slots, ops.ctypes.data_as(C.c_void_p),
+         cap, C.byref(n), C.byref(slots), C.byref(clamped))
+    res = [RingOp(int(k), int(l), int(s), None if w < 0 else int(w))
+           for k, l, s, w in ops[: n.value]]
+    return RingSchedule(res, slots.value, bool(clamped.value))

@@ -1,0 +1,199 @@
+"""Generate tests/golden/*.json from the REFERENCE ITSELF.
+
+Runs oracle/_ref/libmoesim_ref.so — the reference's own collectives.cpp,
+workload.cpp, ring_offload.cpp, sim_engine.cpp and topology.cpp compiled from
+/root/reference/proj by oracle/Makefile — on the cases its own tests pin
+(test_workload.cpp, test_collectives.cpp, test_ring_offload.cpp,
+acceptance_main.cpp) plus config-sized cases, and stores inputs + outputs.
+The GPU box has no /root/reference; the fixtures travel instead.
+
+    make -C oracle ref && python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def sm64(seed):
+    s = C.c_uint64(seed)
+    while True:
+        yield int(oracle.ref().ref_splitmix64_next(C.byref(s)))
+
+
+def random_payload(ranks, seed, max_len=16):
+    """test_collectives.cpp:17-28 random_payload (chunk sizes and bytes from SplitMix64)."""
+    g = sm64(seed)
+    chunks = []
+    for _ in range(ranks * ranks):
+        n = next(g) % (max_len + 1)
+        chunks.append(bytes(next(g) & 0xFF for _ in range(n)))
+    return chunks
+
+
+def ref_a2a(ranks, chunks):
+    r = oracle.ref()
+    lens = np.array([len(c) for c in chunks], dtype=np.uint64)
+    data = np.frombuffer(b"".join(chunks) or b"\0", dtype=np.uint8).copy()
+    out_lens = np.zeros(len(chunks), dtype=np.uint64)
+    out = np.zeros(max(1, int(lens.sum())), dtype=np.uint8)
+    rc = r.ref_alltoall_flat(ranks, len(chunks), oracle.P(lens), oracle.P(data),
+                             oracle.P(out_lens), oracle.P(out))
+    if rc:
+        return {"error": rc}
+    res, o = [], 0
+    for ln in out_lens:
+        res.append(out[o:o + int(ln)].tobytes().hex())
+        o += int(ln)
+    return {"chunks": res}
+
+
+def ref_fuse(slices):
+    r = oracle.ref()
+    n = len(slices)
+    lens = np.array([len(s) for s in slices] or [0], dtype=np.uint64)
+    data = np.frombuffer(b"".join(slices) or b"\0", dtype=np.uint8).copy()
+    blob = np.zeros(max(1, int(lens.sum())), dtype=np.uint8)
+    idx = np.zeros((max(n, 1), 3), dtype=np.uint64)
+    rc = r.ref_fuse_slices(n, oracle.P(lens), oracle.P(data), oracle.P(blob), oracle.P(idx))
+    if rc:
+        return {"error": rc}
+    return {"blob": blob[: int(lens[:n].sum())].tobytes().hex(), "index": idx[:n].tolist()}
+
+
+def ref_split(blob, index):
+    r = oracle.ref()
+    n = len(index)
+    b = np.frombuffer(blob or b"\0", dtype=np.uint8).copy()
+    idx = np.array(index or [[0, 0, 0]], dtype=np.uint64)
+    out = np.zeros(max(1, len(blob)), dtype=np.uint8)
+    rc = r.ref_split_blob(len(blob), oracle.P(b), n, oracle.P(idx), oracle.P(out))
+    if rc:
+        return {"error": rc}
+    res, o = [], 0
+    for (_, _, ln) in index:
+        res.append(out[o:o + ln].tobytes().hex())
+        o += ln
+    return {"slices": res}
+
+
+def ref_schedule(layers, slots):
+    r = oracle.ref()
+    ops = np.zeros((4 * layers + 8, 4), dtype=np.int64)
+    n, k, cl = C.c_uint64(), C.c_uint32(), C.c_int()
+    rc = r.ref_ring_schedule(layers, slots, oracle.P(ops), C.byref(n), C.byref(k), C.byref(cl))
+    if rc:
+        return {"error": rc}
+    return {"ops": ops[: n.value].tolist(), "slots": k.value, "clamped": bool(cl.value)}
+
+
+def ref_simulate(layers, slots, expert_bytes, dense_bytes, compute_ns, bw, lat):
+    r = oracle.ref()
+    comp = np.array(compute_ns, dtype=np.int64)
+    ls, le, cs, ce = (np.zeros(layers, np.int64) for _ in range(4))
+    mk, st, cp = C.c_int64(), C.c_int64(), C.c_int64()
+    pk, bl = C.c_uint64(), C.c_uint64()
+    rc = r.ref_ring_simulate(layers, slots, expert_bytes, dense_bytes, oracle.P(comp), bw, lat,
+                             oracle.P(ls), oracle.P(le), oracle.P(cs), oracle.P(ce), C.byref(mk),
+                             C.byref(st), C.byref(cp), C.byref(pk), C.byref(bl))
+    if rc:
+        return {"error": rc}
+    return {"load_start": ls.tolist(), "load_end": le.tolist(), "compute_start": cs.tolist(),
+            "compute_end": ce.tolist(), "makespan": mk.value, "stall": st.value,
+            "copy_ns": cp.value, "peak_bytes": pk.value, "baseline_bytes": bl.value}
+
+
+def main():
+    assert oracle.ref() is not None, "build the reference first: make -C oracle ref"
+    gold = {"source": "oracle/_ref/libmoesim_ref.so built from /root/reference/proj (see oracle/Makefile)"}
+
+    # rng.hpp:19-42
+    gold["splitmix64"] = [{"seed": s, "draws": [str(v) for v, _ in zip(sm64(s), range(8))]}
+                          for s in (0, 1, 7, 0xC0113C7, 2**64 - 1)]
+    gold["substream_seed"] = [{"args": [s, st, r], "value": str(int(oracle.ref().ref_substream_seed(s, st, r)))}
+                              for s, st, r in ((7, 0, 0), (11, 2, 1), (13, 0, 15), (2**63 + 5, 7, 3))]
+
+    # workload.cpp:19-66 — test_workload.cpp:72-84 cases + config-sized ones
+    traces = []
+    for args in ((7, 1, 2, 4, 100, 0.0), (11, 3, 2, 8, 64, 1.2), (7, 2, 3, 1, 50, 1.5),
+                 (7, 2, 2, 4, 0, 0.0), (42, 4, 4, 16, 256, 0.9), (5, 3, 5, 7, 129, 2.0),
+                 (13, 1, 16, 16, 4096, 0.5),          # scenarios/alltoall_bench.json
+                 (3, 1, 8, 64, 65536, 0.0),           # c2-scale uniform
+                 (3, 1, 8, 32, 65536, 1.2)):          # c3-scale skewed
+        c = oracle.gen_trace(*args, which="ref")
+        ent = {"args": list(args), "counts": c.astype(np.int64).tolist()}
+        if c.sum():
+            ent["imbalance_ratio"] = oracle.imbalance_ratio(c, "ref")
+        traces.append(ent)
+    gold["gen_trace"] = traces
+    gold["imbalance_ratio"] = [
+        {"counts": [[[90, 10]]], "value": 1.8}, {"counts": [[[50, 50]]], "value": 1.0},
+        {"counts": [[[10]]], "value": 1.0}]
+    for ent in gold["imbalance_ratio"]:
+        ent["value"] = oracle.imbalance_ratio(np.array(ent["counts"], dtype=np.uint64), "ref")
+
+    # collectives.cpp:10-21 — test_collectives.cpp:43-66 + acceptance crit 3 style
+    a2a = [{"ranks": 2, "chunks": [b"a".hex(), b"b".hex(), b"c".hex(), b"d".hex()]},
+           {"ranks": 1, "chunks": [bytes([1, 2, 3]).hex()]}]
+    a2a.append({"ranks": 4, "chunks": [c.hex() for c in random_payload(4, 99)]})
+    for r, seed in ((3, 5), (8, 1234), (5, 0xC0113C7)):
+        a2a.append({"ranks": r, "chunks": [c.hex() for c in random_payload(r, seed, 64)]})
+    a2a.append({"ranks": 2, "chunks": ["aa", "bb", "cc"]})  # non-square -> invalid_argument
+    for ent in a2a:
+        ent["expected"] = ref_a2a(ent["ranks"], [bytes.fromhex(c) for c in ent["chunks"]])
+    gold["alltoall_flat"] = a2a
+
+    # collectives.cpp:88-118 — test_collectives.cpp:136-171
+    fuse = [[bytes([1, 2, 3])], [bytes([1, 2, 3]), b"", bytes([4, 5, 6, 7, 8])], []]
+    g = sm64(17)
+    for _ in range(6):
+        sl = []
+        for _ in range(1 + next(g) % 8):
+            sl.append(bytes(next(g) & 0xFF for _ in range(next(g) % 12)))
+        fuse.append(sl)
+    gold["fuse_slices"] = [{"slices": [s.hex() for s in sl], "expected": ref_fuse(sl)} for sl in fuse]
+    split = [
+        {"blob": bytes([1, 2]).hex(), "index": [[0, 0, 2]]},
+        {"blob": bytes([1, 2, 0]).hex(), "index": [[0, 0, 2]]},      # longer blob -> error
+        {"blob": bytes([1, 2]).hex(), "index": [[0, 1, 2]]},         # gap -> error
+        {"blob": bytes(range(8)).hex(), "index": [[0, 0, 3], [1, 3, 0], [2, 3, 5]]},
+    ]
+    for ent in split:
+        ent["expected"] = ref_split(bytes.fromhex(ent["blob"]), ent["index"])
+    gold["split_blob"] = split
+
+    # ring_offload.cpp:31-117 — test_ring_offload.cpp:29-152, scenarios/infer_ring.json
+    gold["ring_schedule"] = [{"args": [n, k], "expected": ref_schedule(n, k)}
+                             for n, k in ((1, 1), (3, 1), (4, 2), (3, 10), (24, 2), (12, 2), (4, 0))]
+    sec = 1_000_000_000
+    sims = [
+        (24, 2, 1000, 0, [2 * sec] * 24, 1000, 0),
+        (5, 2, 0, 0, [3 * sec] * 5, 1000, 0),
+        (6, 6, 1000, 0, [2 * sec] * 6, 1000, 0),
+        (5, 1, 800, 0, [sec] * 5, 1000, 0),
+        (5, 3, 800, 0, [sec] * 5, 1000, 0),
+        (8, 3, 5000, 0, [sec] * 8, 1000, 0),
+        (24, 2, 50_000_000, 120_000_000, [2_500_000] * 24, 25_000_000_000, 2000),
+        (12, 2, 2_147_483_648, 1_000_000, [40_000_000 + 1_000_000 * i for i in range(12)],
+         55_000_000_000, 2000),
+    ]
+    gold["ring_simulate"] = [{"args": list(a[:4]) + [a[4], a[5], a[6]],
+                              "expected": ref_simulate(*a)} for a in sims]
+
+    with open(os.path.join(OUT, "reference_golden.json"), "w") as f:
+        json.dump(gold, f, indent=1, sort_keys=True)
+    print("wrote", os.path.join(OUT, "reference_golden.json"))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,190 @@
+"""GPU: K5 grouped GEMM (tcgen05 bf16 and SIMT fp32) against a torch fp32
+reference of the same op, for every layout/epilogue the layer uses, with
+ragged/empty groups and row masking."""
+import ctypes as C
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2205_10034_b200 import _lib, grouped_gemm  # noqa: E402
+from paper_2205_10034_b200._lib import GemmProblem  # noqa: E402
+
+dev = torch.device("cuda")
+
+
+def gelu(h):
+    return 0.5 * h * (1.0 + torch.erf(h * 0.7071067811865476))
+
+
+def gelu_grad(h):
+    return 0.5 * (1.0 + torch.erf(h * 0.7071067811865476)) + h * 0.3989422804014327 * torch.exp(-0.5 * h * h)
+
+
+def i32(v):
+    return torch.tensor(v, dtype=torch.int32, device=dev)
+
+
+def ragged_m_case(dtype, b_mn, epi, N=512, K=256, groups=(200, 0, 128, 37, 300), bvec=(0, 1, 2, 1, 0),
+                  Cs=320, bias=True, out_f32=False):
+    torch.manual_seed(0)
+    G = len(groups)
+    nb = max(bvec) + 1
+    rows = G * Cs
+    A = (torch.rand(rows, K, device=dev) * 2 - 1).to(dtype)
+    W = (torch.rand(nb, N, K, device=dev) * 2 - 1) / K ** 0.5  # [b][N][K]
+    Bmat = W.to(dtype)
+    Bstore = Bmat.transpose(1, 2).contiguous() if b_mn else Bmat.contiguous()
+    bias_t = torch.rand(nb, N, device=dev) - 0.5 if bias else None
+    cdt = torch.float32 if (out_f32 or dtype == torch.float32) else dtype
+    Cm = torch.full((rows, N), 7.0, device=dev, dtype=cdt)
+    C2 = torch.full((rows, N), 7.0, device=dev, dtype=cdt)
+    aux = (torch.rand(rows, N, device=dev) * 4 - 2).to(cdt)
+    m, a_row, b = i32(list(groups)), i32([g * Cs for g in range(G)]), i32(list(bvec))
+    p = GemmProblem()
+    p.kind = _lib.MOE_GEMM_RAGGED_M
+    p.epilogue = epi
+    p.dtype_ab = _lib.MOE_DTYPE_BF16 if dtype == torch.bfloat16 else _lib.MOE_DTYPE_F32
+    p.dtype_c = _lib.MOE_DTYPE_F32 if cdt == torch.float32 else _lib.MOE_DTYPE_BF16
+    p.b_mn_major = 1 if b_mn else 0
+    p.groups, p.N, p.K, p.a_rows, p.num_b = G, N, K, rows, nb
+    p.m, p.a_row, p.c_row, p.b = m.data_ptr(), a_row.data_ptr(), a_row.data_ptr(), b.data_ptr()
+    p.A, p.B, p.C = A.data_ptr(), Bstore.data_ptr(), Cm.data_ptr()
+    p.C2 = C2.data_ptr()
+    p.aux = aux.data_ptr()
+    p.bias = bias_t.data_ptr() if bias_t is not None else None
+    p.ldc = N
+    grouped_gemm(p)
+    torch.cuda.synchronize()
+    # reference
+    refC = torch.full((rows, N), 7.0, device=dev)
+    refC2 = torch.full((rows, N), 7.0, device=dev)
+    for g in range(G):
+        r0, mm = g * Cs, groups[g]
+        if mm == 0:
+            continue
+        acc = A[r0:r0 + mm].float() @ Bmat[bvec[g]].float().t()
+        if epi == _lib.MOE_EPI_DGELU:
+            acc = acc * gelu_grad(aux[r0:r0 + mm].float())
+        elif bias_t is not None:
+            acc = acc + bias_t[bvec[g]]
+        if epi == _lib.MOE_EPI_GELU:
+            refC2[r0:r0 + mm] = acc
+            acc = gelu(acc)
+        refC[r0:r0 + mm] = acc
+    return Cm.float(), refC, C2.float(), refC2
+
+
+def assert_close(got, ref, rel):
+    scale = ref[ref != 7.0].abs().max().clamp_min(1e-6) if (ref != 7.0).any() else torch.tensor(1.0)
+    err = (got - ref).abs().max()
+    assert err <= rel * scale, f"max err {err.item()} vs scale {scale.item()}"
+
+
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("out_f32", [False, True])
+def test_tc_ragged_m_store(b_mn, out_f32):
+    got, ref, _, _ = ragged_m_case(torch.bfloat16, b_mn, _lib.MOE_EPI_STORE, out_f32=out_f32)
+    assert_close(got, ref, 1e-2)
+    assert (got[ref == 7.0] == 7.0).all()  # rows past m[g] untouched
+
+
+def test_tc_ragged_m_gelu():
+    got, ref, got2, ref2 = ragged_m_case(torch.bfloat16, False, _lib.MOE_EPI_GELU)
+    assert_close(got, ref, 1e-2)
+    assert_close(got2, ref2, 1e-2)
+
+
+def test_tc_ragged_m_dgelu():
+    got, ref, _, _ = ragged_m_case(torch.bfloat16, True, _lib.MOE_EPI_DGELU, bias=False)
+    assert_close(got, ref, 1e-2)
+
+
+def test_tc_small_n_masked():
+    """gate-logits shape: N = 32 < BN = 64, K-major B, fp32 out."""
+    got, ref, _, _ = ragged_m_case(torch.bfloat16, False, _lib.MOE_EPI_STORE, N=32, K=128,
+                                   groups=(1000,), bvec=(0,), Cs=1000, out_f32=True)
+    assert_close(got, ref, 1e-2)
+
+
+def test_tc_large_k():
+    got, ref, _, _ = ragged_m_case(torch.bfloat16, False, _lib.MOE_EPI_STORE, N=256, K=2048,
+                                   groups=(129, 255), bvec=(0, 1), Cs=256)
+    assert_close(got, ref, 1e-2)
+
+
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("epi", [0, 1, 2])
+def test_simt_ragged_m(b_mn, epi):
+    if epi == 1 and b_mn:
+        pytest.skip("layer uses GELU with K-major B only")
+    got, ref, got2, ref2 = ragged_m_case(torch.float32, b_mn, epi, N=192, K=96,
+                                         bias=(epi != 2))
+    assert_close(got, ref, 2e-6)
+    if epi == 1:
+        assert_close(got2, ref2, 2e-6)
+
+
+def ragged_k_case(dtype, atomic, M=256, N=512, groups=(100, 0, 64, 300, 17), bvec=(0, 0, 1, 1, 2),
+                  Cs=320, transpose=False):
+    torch.manual_seed(1)
+    G = len(groups)
+    nb = max(bvec) + 1
+    rows = G * Cs
+    A = (torch.rand(rows, M, device=dev) * 2 - 1).to(dtype)
+    B = (torch.rand(rows, N, device=dev) * 2 - 1).to(dtype)
+    for g in range(G):  # zero pad rows (the layer guarantees this up to 64)
+        A[g * Cs + groups[g]:(g + 1) * Cs] = 0
+    if atomic:
+        out = torch.zeros(nb * (N if transpose else M), M if transpose else N, device=dev)
+    else:
+        out = torch.full((nb * M, N), 7.0, device=dev)
+    m, a_row, b = i32(list(groups)), i32([g * Cs for g in range(G)]), i32(list(bvec))
+    p = GemmProblem()
+    p.kind = _lib.MOE_GEMM_RAGGED_K
+    p.epilogue = _lib.MOE_EPI_ATOMIC_ADD if atomic else _lib.MOE_EPI_STORE
+    p.dtype_ab = _lib.MOE_DTYPE_BF16 if dtype == torch.bfloat16 else _lib.MOE_DTYPE_F32
+    p.dtype_c = _lib.MOE_DTYPE_F32
+    p.transpose_c = 1 if transpose else 0
+    p.groups, p.M, p.N, p.a_rows, p.num_b = G, M, N, rows, nb
+    p.m, p.a_row, p.b = m.data_ptr(), a_row.data_ptr(), b.data_ptr()
+    p.A, p.B, p.C = A.data_ptr(), B.data_ptr(), out.data_ptr()
+    p.ldc = M if transpose else N
+    grouped_gemm(p)
+    torch.cuda.synchronize()
+    ref = torch.zeros(nb, M, N, device=dev)
+    for g in range(G):
+        r0, mm = g * Cs, groups[g]
+        ref[bvec[g]] += A[r0:r0 + mm].float().t() @ B[r0:r0 + mm].float()
+    if transpose:
+        ref = ref.transpose(1, 2).reshape(nb * N, M)
+    else:
+        ref = ref.reshape(nb * M, N)
+    return out, ref
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_ragged_k_store(dtype):
+    got, ref = ragged_k_case(dtype, atomic=False)
+    assert_close(got, ref, 1e-2 if dtype == torch.bfloat16 else 2e-6)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_ragged_k_atomic_transposed(dtype):
+    """gate weight-gradient shape: N = E = 64 (BN=64 path), split-K groups, C^T."""
+    got, ref = ragged_k_case(dtype, atomic=True, M=256, N=64, groups=(64, 64, 40, 128),
+                             bvec=(0, 0, 0, 0), Cs=128, transpose=True)
+    assert_close(got, ref, 1e-2 if dtype == torch.bfloat16 else 2e-6)
+
+
+def test_tc_many_groups_persistent_schedule():
+    """More tiles than SMs, many groups, so the persistent scheduler wraps."""
+    groups = tuple((i * 37) % 300 for i in range(64))
+    bvec = tuple(i % 8 for i in range(64))
+    got, ref, _, _ = ragged_m_case(torch.bfloat16, False, _lib.MOE_EPI_STORE, N=1024, K=128,
+                                   groups=groups, bvec=bvec, Cs=320)
+    assert_close(got, ref, 1e-2)

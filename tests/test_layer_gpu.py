@@ -1,0 +1,176 @@
+"""GPU: the full MoE layer (forward + backward) through the C-ABI against the
+fp64 CPU oracle (DESIGN.md Appendix A) on identical SplitMix64-generated
+inputs.  Routing integers must be bit-exact given the GPU's fp32 logits;
+float outputs and gradients within the north-star tolerances:
+    fp32: max|got - ref| <= 1e-5 * max|ref|    (per tensor)
+    bf16: max|got - ref| <= 2e-2 * max|ref|    (oracle emulates the bf16 stores)
+At full config size the oracle is too slow; there a torch fp32 reference of
+the same layer, built on the GPU's own routing, checks the numerics."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2205_10034_b200 import MoEConfig, MoELayer  # noqa: E402
+from paper_2205_10034_b200.layer import T_DY  # noqa: E402
+
+TOL = {torch.float32: 1e-5, torch.bfloat16: 2e-2}
+
+
+def rel_err(got, ref):
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def run_case(E, k, d, dff, T, cf, dtype, seed=1234, d_aux=0.05, gate_bias=None):
+    cfg = MoEConfig(E, k, d, dff, cf, T, dtype, gate_bias=gate_bias is not None)
+    layer = MoELayer(cfg)
+    gb = None if gate_bias is None else torch.tensor(gate_bias, dtype=torch.float32).cuda()
+    layer.init_params(seed, gate_bias=gb)
+    x = layer.make_input(seed)
+    dy = layer.make_input(seed, T_DY)
+    y, rout = layer.forward(x, routing=True)
+    dx = layer.backward(dy, d_aux=d_aux)
+    torch.cuda.synchronize()
+    bf16 = dtype == torch.bfloat16
+    ref_t = oracle.make_layer_tensors(seed, T, d, dff, E, bf16, gate_bias=gate_bias)
+    # inputs are bit-identical
+    assert np.array_equal(x.float().cpu().numpy(), ref_t["x"])
+    assert np.array_equal(layer.params["w1"].float().cpu().numpy(), ref_t["w1"])
+    g_logits = rout["logits"].cpu().numpy()
+    fwd = oracle.moe_forward(ref_t["x"], ref_t["wg"], ref_t["bg"], ref_t["w1"], ref_t["b1"],
+                             ref_t["w2"], ref_t["b2"], k, layer.capacity, bf16,
+                             logits_in=g_logits)
+    fwd["logits_used"] = g_logits
+    return layer, x, y, dx, rout, fwd, ref_t, d_aux
+
+
+def check_case(E, k, d, dff, T, cf, dtype, **kw):
+    layer, x, y, dx, rout, fwd, ref_t, d_aux = run_case(E, k, d, dff, T, cf, dtype, **kw)
+    tol = TOL[dtype]
+    # K1: logits vs fp64-accumulated logits
+    assert rel_err(rout["logits"].cpu().numpy(), fwd["logits"]) < (1e-5 if dtype == torch.float32 else 1e-4)
+    # K2: routing bit-exact given the GPU logits
+    for n in ("expert", "position", "count1", "count2", "kept", "keep"):
+        assert np.array_equal(rout[n].cpu().numpy(), fwd[n]), n
+    np.testing.assert_allclose(rout["gate"].cpu().numpy(), fwd["gate"], rtol=2e-6, atol=1e-7)
+    np.testing.assert_allclose(rout["aux_loss"].item(), fwd["aux_loss"], rtol=1e-5)
+    # forward output
+    assert rel_err(y.float().cpu().numpy(), fwd["y"]) <= tol
+    # backward
+    bwd = oracle.moe_backward(ref_t["x"], ref_t["wg"], ref_t["bg"], ref_t["w1"], ref_t["b1"],
+                              ref_t["w2"], ref_t["b2"], k, layer.capacity, dtype == torch.bfloat16,
+                              fwd, ref_t["dy"], d_aux)
+    g = layer.grads
+    checks = {
+        "dx": (dx.float().cpu().numpy(), bwd["dx"]),
+        "dwg": (g["dwg"].cpu().numpy(), bwd["dwg"]),
+        "dw1": (g["dw1"].cpu().numpy(), bwd["dw1"]),
+        "db1": (g["db1"].cpu().numpy(), bwd["db1"]),
+        "dw2": (g["dw2"].cpu().numpy(), bwd["dw2"]),
+        "db2": (g["db2"].cpu().numpy(), bwd["db2"]),
+    }
+    if kw.get("gate_bias") is not None:
+        checks["dbg"] = (g["dbg"].cpu().numpy(), bwd["dbg"])
+    errs = {n: rel_err(a, b) for n, (a, b) in checks.items()}
+    bad = {n: e for n, e in errs.items() if not e <= tol}
+    assert not bad, errs
+    return layer, fwd
+
+
+def test_layer_bf16_top2_small():
+    check_case(E=8, k=2, d=256, dff=512, T=512, cf=1.25, dtype=torch.bfloat16)
+
+
+def test_layer_bf16_top1_switch_shape():
+    # config c2 ratios (E=64, top-1, d_ff = 4 d) at reduced size
+    check_case(E=64, k=1, d=128, dff=512, T=2048, cf=1.25, dtype=torch.bfloat16)
+
+
+def test_layer_bf16_skewed_drops_c3():
+    E = 32
+    bias = [-1.2 * np.log(e + 1.0) for e in range(E)]
+    layer, fwd = check_case(E=E, k=2, d=128, dff=256, T=1024, cf=1.25, dtype=torch.bfloat16,
+                            gate_bias=bias)
+    assert (fwd["keep"] == 0).sum() > 0  # capacity drops exercised
+
+
+def test_layer_fp32_c1_shape():
+    # config c1 (E=8 top-2 d=512 d_ff=2048 cf=1.25, fp32) at T=512 (oracle cost)
+    check_case(E=8, k=2, d=512, dff=2048, T=512, cf=1.25, dtype=torch.float32)
+
+
+def test_layer_fp32_drops():
+    check_case(E=4, k=2, d=64, dff=128, T=300, cf=0.5, dtype=torch.float32)
+
+
+def test_layer_ragged_tokens_bf16():
+    # T not a multiple of the routing chunk / GEMM tile, tiny experts
+    check_case(E=16, k=2, d=128, dff=256, T=333, cf=2.0, dtype=torch.bfloat16)
+
+
+# ---------------------------------------------------------------- full size --
+def torch_reference(layer, x, dy, rout, d_aux):
+    """fp32 torch restatement of Appendix A on the GPU's routing (for sizes the
+    CPU oracle cannot finish)."""
+    p = layer.params
+    c = layer.cfg
+    T, E, k = c.tokens, c.num_experts, c.top_k
+    xf = x.float().requires_grad_(True)
+    wg = p["wg"].float().requires_grad_(True)
+    w1 = p["w1"].float().requires_grad_(True)
+    b1 = p["b1"].clone().requires_grad_(True)
+    w2 = p["w2"].float().requires_grad_(True)
+    b2 = p["b2"].clone().requires_grad_(True)
+    logits = xf @ wg.t()
+    prob = torch.softmax(logits, dim=-1)
+    e_idx = rout["expert"].long()
+    keep = rout["keep"].bool()
+    if k == 1:
+        g = prob.gather(1, e_idx)
+    else:
+        pe = prob.gather(1, e_idx)
+        g = pe / pe.sum(1, keepdim=True)
+    count1 = torch.bincount(e_idx[:, 0], minlength=E).float()
+    aux = E * ((prob.mean(0)) * (count1 / T)).sum()
+    y = torch.zeros(T, c.d_model, device=x.device)
+    for e in range(E):
+        for i in range(k):
+            sel = (e_idx[:, i] == e) & keep[:, i]
+            if sel.any():
+                h = xf[sel] @ w1[e].t() + b1[e]
+                a = 0.5 * h * (1 + torch.erf(h * 0.7071067811865476))
+                ye = a @ w2[e].t() + b2[e]
+                y = y.index_add(0, sel.nonzero().squeeze(1), g[sel, i:i + 1] * ye)
+    loss = (y * dy.float()).sum() + d_aux * aux
+    loss.backward()
+    return y.detach(), xf.grad, wg.grad, w1.grad, b1.grad, w2.grad, b2.grad
+
+
+@pytest.mark.parametrize("E,k,d,dff,T", [(64, 1, 1024, 4096, 65536), (32, 2, 1024, 4096, 16384)])
+def test_layer_full_size_vs_torch_fp32(E, k, d, dff, T):
+    cfg = MoEConfig(E, k, d, dff, 1.25, T, torch.bfloat16)
+    layer = MoELayer(cfg)
+    layer.init_params(7)
+    x = layer.make_input(7)
+    dy = layer.make_input(7, T_DY)
+    y, rout = layer.forward(x, routing=True)
+    dx = layer.backward(dy, d_aux=0.01)
+    torch.cuda.synchronize()
+    ry, rdx, rdwg, rdw1, rdb1, rdw2, rdb2 = torch_reference(layer, x, dy, rout, 0.01)
+    g = layer.grads
+
+    def err(a, b):
+        return ((a.float() - b).abs().max() / b.abs().max()).item()
+
+    errs = {"y": err(y, ry), "dx": err(dx, rdx), "dwg": err(g["dwg"], rdwg),
+            "dw1": err(g["dw1"], rdw1), "db1": err(g["db1"], rdb1), "dw2": err(g["dw2"], rdw2),
+            "db2": err(g["db2"], rdb2)}
+    assert all(v <= 2e-2 for v in errs.values()), errs
