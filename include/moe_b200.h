@@ -162,10 +162,13 @@ moe_status_t moe_route(uint64_t tokens, uint32_t experts, uint32_t top_k, uint64
  * Group tables are device int32 arrays of length `groups`. */
 typedef enum moe_gemm_kind { MOE_GEMM_RAGGED_M = 0, MOE_GEMM_RAGGED_K = 1 } moe_gemm_kind_t;
 typedef enum moe_gemm_epilogue {
-  MOE_EPI_STORE = 0,      /* C = acc (+bias) in dtype_c                       */
-  MOE_EPI_GELU = 1,       /* C = act(acc+bias), C2 = acc+bias (pre-activation) */
-  MOE_EPI_DGELU = 2,      /* C = acc * gelu'(AUX[row, n])                      */
-  MOE_EPI_ATOMIC_ADD = 3  /* fp32 C += acc (split-K); transpose_c allowed       */
+  MOE_EPI_STORE = 0,      /* C = acc (+bias) in dtype_c                                */
+  MOE_EPI_GELU = 1,       /* h = acc+bias: C = gelu(h), C2 = gelu'(h) (erf GeLU)        */
+  MOE_EPI_DGELU = 2,      /* C = acc * AUX[row, n] (AUX = the gelu'(h) C2 stored);
+                             colsum (optional) += column sums of the stored C           */
+  MOE_EPI_ATOMIC_ADD = 3, /* fp32 C += acc (split-K); transpose_c allowed               */
+  MOE_EPI_GATHER_ADD = 4  /* C[t] = acc + sum_i gather_src[gather_idx[t*k+i]] (idx -1
+                             skipped): combine-backward folded into the gate dgrad GEMM  */
 } moe_gemm_epilogue_t;
 
 typedef struct moe_gemm_problem {
@@ -193,6 +196,11 @@ typedef struct moe_gemm_problem {
   uint64_t lda;           /* A row stride in elements (0: K for RAGGED_M, M for RAGGED_K) */
   uint64_t ldb;           /* B row stride in elements (0: natural) */
   uint64_t b_rows;        /* rows allocated in B (0: num_b * (N or K), RAGGED_K: a_rows) */
+  uint64_t c_rows;        /* rows allocated in C (0: a_rows for RAGGED_M)                */
+  float* colsum;          /* DGELU: [num_b][N] fp32 accumulated column sums, or NULL     */
+  const void* gather_src; /* GATHER_ADD: [*, N] rows in dtype_c                          */
+  const int32_t* gather_idx; /* GATHER_ADD: [rows][gather_k] row indices or -1          */
+  uint32_t gather_k;
 } moe_gemm_problem_t;
 
 moe_status_t moe_grouped_gemm(const moe_gemm_problem_t* problem, void* stream);

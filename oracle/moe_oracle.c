@@ -502,8 +502,8 @@ int oracle_moe_backward(uint64_t T, uint32_t d, uint32_t dff, uint32_t E, uint32
         for (uint32_t j = 0; j < dff; ++j) {
           double acc = 0.0;
           for (uint32_t o = 0; o < d; ++o) acc += dyv[o] * (double)W2[(uint64_t)o * dff + j];
-          /* gelu' evaluated on the stored pre-activation H */
-          dh[j] = rnd(acc * gelu_grad(rnd(hpre[j], B)), B);
+          /* gelu'(h) as stored by the forward epilogue (rounded), then dH stored */
+          dh[j] = rnd(acc * rnd(gelu_grad(hpre[j]), B), B);
           db1[(uint64_t)e * dff + j] += dh[j];
         }
         for (uint32_t j = 0; j < dff; ++j) {

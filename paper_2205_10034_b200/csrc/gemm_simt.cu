@@ -21,6 +21,10 @@ struct Args {
   const float* bias;
   long long lda, ldb, ldc;
   long long b_rows;
+  float* colsum;
+  const float* gsrc;
+  const int* gidx;
+  int gk;
 };
 
 __global__ void __launch_bounds__(THREADS) simt_gemm_kernel(const Args a) {
@@ -158,13 +162,20 @@ __global__ void __launch_bounds__(THREADS) simt_gemm_kernel(const Args a) {
           atomicAdd(a.C + idx, v);
           continue;
         }
-        if (a.bias && a.epi != MOE_EPI_DGELU) v += a.bias[(long long)bidx * a.N + n];
+        if (a.bias && a.epi != MOE_EPI_DGELU && a.epi != MOE_EPI_GATHER_ADD)
+          v += a.bias[(long long)bidx * a.N + n];
         const long long idx = orow * a.ldc + n;
         if (a.epi == MOE_EPI_GELU) {
-          a.C2[idx] = v;
+          a.C2[idx] = gelu_grad_f(v);  // stored derivative gelu'(h)
           v = gelu_f(v);
         } else if (a.epi == MOE_EPI_DGELU) {
-          v *= gelu_grad_f(a.aux[idx]);
+          v *= a.aux[idx];
+          if (a.colsum) atomicAdd(a.colsum + (long long)bidx * a.N + n, v);
+        } else if (a.epi == MOE_EPI_GATHER_ADD) {
+          for (int i = 0; i < a.gk; ++i) {
+            const int s = a.gidx[orow * a.gk + i];
+            if (s >= 0) v += a.gsrc[(long long)s * a.N + n];
+          }
         }
         a.C[idx] = v;
       }
@@ -198,6 +209,10 @@ void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
   a.C2 = static_cast<float*>(p.C2);
   a.aux = static_cast<const float*>(p.aux);
   a.bias = p.bias;
+  a.colsum = p.colsum;
+  a.gsrc = static_cast<const float*>(p.gather_src);
+  a.gidx = p.gather_idx;
+  a.gk = (int)p.gather_k;
   a.ldc = (long long)p.ldc;
   if (p.kind == MOE_GEMM_RAGGED_M) {
     a.lda = p.lda ? p.lda : p.K;

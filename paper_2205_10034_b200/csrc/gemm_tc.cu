@@ -1,12 +1,15 @@
 // K5 — grouped expert GEMM on 5th-generation tensor cores (sm_100a).
 //
-// One persistent, warp-specialised kernel per shape class:
-//   warp 0      TMA producer (one lane): A/B tiles -> 128B-swizzled smem ring
-//   warp 1      MMA issuer  (one lane): tcgen05.mma 128xBNx16, fp32 accum in TMEM
-//   warp 2      TMEM allocator (2 x BN columns: double-buffered accumulator)
-//   warps 4..7  epilogue: tcgen05.ld 32 lanes x 32 columns -> bias/GeLU/GeLU'
-//               -> bf16/fp32 stores (or fp32 atomics for split-K)
-// Work items are read from device-side group tables (no host sync on routing
+// One persistent, warp-specialised kernel per shape class (384 threads):
+//   warp 0       TMA producer (one lane): A/B tiles -> 128B-swizzled smem ring
+//   warp 1       MMA issuer  (one lane): tcgen05.mma 128xBNx16, fp32 accum in TMEM
+//   warp 2       TMEM allocator (2 x BN columns: double-buffered accumulator)
+//   warps 4..11  epilogue: warp w owns TMEM lanes 32*(w%4).. and half the columns;
+//                tcgen05.ld -> bias / GeLU / GeLU' / gather-add -> bf16|fp32 ->
+//                64B-swizzled smem staging -> TMA bulk tensor store (partial
+//                row blocks fall back to masked stores); GeLU' operands arrive
+//                by TMA one chunk ahead; optional fused column sums (bias grad).
+// Work items come from device-side group tables (no host sync on routing
 // counts — the paper's CPU-side scheduling overhead):
 //   RAGGED_M : group g = one (source, expert) slice of m[g] rows; tiles =
 //              ceil(m/128) x ceil(N/BN); B = the expert's weight (K- or MN-major)
@@ -28,22 +31,30 @@ namespace tc {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int THREADS = 256;
+constexpr int THREADS = 384;
+constexpr int EPI_WARPS = 8;
 constexpr int MAX_GROUPS = 1024;
+constexpr int STG = 2048;  // one 32-row x 64B staging tile
 
-template <int BN>
+template <int BN, int EPI, bool CF32>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES =
+      (BN == 256) ? ((EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU) ? 3 : 4) : (BN == 128 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN;
-  // smem: stages | barriers | tmem holder | tables
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int BAR_BYTES = (2 * STAGES + 4) * 8;
+  static constexpr int CW = CF32 ? 16 : 32;  // epilogue chunk width (columns): 64B per row
+  static constexpr int NOUT = (EPI == MOE_EPI_GELU) ? 2 : 1;
+  static constexpr int NAUX = (EPI == MOE_EPI_DGELU) ? 2 : 0;
+  static constexpr int WARP_EPI_BYTES = (NOUT + NAUX) * STG;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = EPI_OFF + EPI_WARPS * WARP_EPI_BYTES;
+  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * EPI_WARPS) * 8;
   static constexpr int HOLD_OFF = BAR_OFF + BAR_BYTES;
   static constexpr int TAB_OFF = ((HOLD_OFF + 16 + 15) / 16) * 16;
   static constexpr int SMEM = TAB_OFF + (MAX_GROUPS + 1) * 4 + 1024;  // + alignment slack
+  static_assert(SMEM <= 232448, "smem budget");
 };
 
 struct Args {
@@ -55,8 +66,11 @@ struct Args {
   const int* gb;
   void* C;
   void* C2;
-  const __nv_bfloat16* aux;
   const float* bias;
+  float* colsum;
+  const void* gsrc;
+  const int* gidx;
+  int gk;
   long long ldc;
   int transpose_c;
   int num_b;
@@ -84,11 +98,70 @@ __device__ void warp_scan_smem(const int* vals, int n, int* out) {
   if (lane == 31) out[n] = incl;
 }
 
+// write 32 values (bf16: 32 cols = 4 x 16B) or 16 (fp32: 16 cols = 4 x 16B)
+// of row r into a 64B-row SWIZZLE_64B staging tile
+template <bool CF32>
+__device__ __forceinline__ void stage_row(uint8_t* stg, uint32_t r, const float* f) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 o;
+    if (CF32) {
+      o = make_uint4(__float_as_uint(f[j * 4 + 0]), __float_as_uint(f[j * 4 + 1]),
+                     __float_as_uint(f[j * 4 + 2]), __float_as_uint(f[j * 4 + 3]));
+    } else {
+      o.x = pack_bf16x2(f[j * 8 + 0], f[j * 8 + 1]);
+      o.y = pack_bf16x2(f[j * 8 + 2], f[j * 8 + 3]);
+      o.z = pack_bf16x2(f[j * 8 + 4], f[j * 8 + 5]);
+      o.w = pack_bf16x2(f[j * 8 + 6], f[j * 8 + 7]);
+    }
+    *reinterpret_cast<uint4*>(stg + sw64(r, j)) = o;
+  }
+}
+
+// masked direct store of one row's chunk (partial tiles)
+template <bool CF32>
+__device__ __forceinline__ void store_row_direct(void* base, long long off, int ncols,
+                                                 const float* f) {
+  constexpr int CW = CF32 ? 16 : 32;
+  if (CF32) {
+    float* p = reinterpret_cast<float*>(base) + off;
+    if (ncols >= CW) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<float4*>(p + q * 4) =
+            make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < CW; ++i)
+        if (i < ncols) p[i] = f[i];
+    }
+  } else {
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(base) + off;
+    if (ncols >= CW) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 o;
+        o.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
+        o.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
+        o.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
+        o.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
+        *reinterpret_cast<uint4*>(p + q * 8) = o;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < CW; ++i)
+        if (i < ncols) p[i] = f2bf(f[i]);
+    }
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const Args args) {
-  using C_ = Cfg<BN>;
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
+                   const __grid_constant__ CUtensorMap tmAux, const Args args) {
+  using C_ = Cfg<BN, EPI, CF32>;
+  constexpr int CW = C_::CW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -96,6 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* empty = full + C_::STAGES;
   uint64_t* tfull = empty + C_::STAGES;
   uint64_t* tempty = tfull + 2;
+  uint64_t* abar = tempty + 2;  // [EPI_WARPS][2] aux-tile arrival barriers
   uint32_t* tmem_hold = reinterpret_cast<uint32_t*>(smem + C_::HOLD_OFF);
   int* tab = reinterpret_cast<int*>(smem + C_::TAB_OFF);  // [MAX_GROUPS+1]
 
@@ -116,17 +190,15 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], EPI_WARPS);
     }
+    for (int a = 0; a < 2 * EPI_WARPS; ++a) mbar_init(&abar[a], 1);
     fence_mbar_init();
   }
   if (warp == 2) {
     tmem_alloc(tmem_hold, C_::TMEM_COLS);
     tc_fence_before();
   }
-  // Work tables: RAGGED_M -> tab = exclusive prefix of tiles per group;
-  // RAGGED_K -> tab = first group of each segment (segment = output run,
-  // or single group in atomic split-K mode).
   int* scratch = reinterpret_cast<int*>(smem);  // stage 0 is free during setup
   if (KIND == 0) {
     for (int g = threadIdx.x; g < G; g += THREADS) {
@@ -144,13 +216,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (KIND == 0) {
       warp_scan_smem(scratch, G, tab);
     } else {
-      // positions of segment starts: exclusive scan of flags, then compact
       int* pos = scratch + MAX_GROUPS + 1;
       warp_scan_smem(scratch, G, pos);
       __syncwarp();
       for (int g = lane; g < G; g += 32)
         if (scratch[g]) tab[pos[g]] = g;
-      if (lane == 0) tab[pos[G]] = G;  // sentinel: nseg = pos[G]
+      if (lane == 0) tab[pos[G]] = G;
       if (lane == 0) tab[MAX_GROUPS] = pos[G];
     }
   }
@@ -159,24 +230,17 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem_base = *tmem_hold;
 
   int total_work;
-  int nseg = 0;
   const int mt = args.M / BM;  // RAGGED_K only
-  if (KIND == 0) {
-    total_work = tab[G];
-  } else {
-    nseg = tab[MAX_GROUPS];
-    total_work = nseg * mt * nblk_n;
-  }
+  if (KIND == 0) total_work = tab[G];
+  else total_work = tab[MAX_GROUPS] * mt * nblk_n;
 
-  // decode a work item
   auto decode = [&](int w, int& g, int& mb, int& nb) {
     if (KIND == 0) {
-      int lo = 0, hi = G;  // last g with tab[g] <= w
+      int lo = 0, hi = G;  // last g with tab[g] <= w (skips empty groups)
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
         if (tab[mid] <= w) lo = mid; else hi = mid;
       }
-      // skip empty groups with equal prefix
       g = lo;
       const int local = w - tab[g];
       mb = local / nblk_n;
@@ -278,120 +342,161 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    // ================= epilogue =================
-    const int ew = warp - 4;          // TMEM lanes 32*ew .. 32*ew+31
-    const int r = ew * 32 + lane;     // row within the tile
+    // ================= epilogue (8 warps) =================
+    const int ew = warp - 4;
+    const int q = warp & 3;           // TMEM lane quarter (hardware: warp % 4)
+    const int half = ew >> 2;         // column half of the tile
+    constexpr int HALF = BN / 2;
+    constexpr int NCH = (HALF + CW - 1) / CW;
+    uint8_t* stg = smem + C_::EPI_OFF + ew * C_::WARP_EPI_BYTES;  // out [, out2] [, aux0, aux1]
+    uint8_t* stg2 = stg + STG;
+    uint8_t* auxb = stg + C_::NOUT * STG;
+    uint64_t* ab = abar + 2 * ew;
+    uint32_t aph[2] = {0, 0};
     uint32_t tcount = 0;
     for (int w = blockIdx.x; w < total_work; w += gridDim.x, ++tcount) {
       int g, mb, nb;
       decode(w, g, mb, nb);
+      const int row0 = mb * BM + q * 32;  // first tile row of this warp
+      int nvalid, bidx;
+      long long orow0;
+      if (KIND == 0) {
+        nvalid = min(32, max(0, args.gm[g] - row0));
+        orow0 = (long long)args.gc[g] + row0;
+        bidx = args.gb[g];
+      } else {
+        nvalid = 32;
+        bidx = args.gb[tab[g]];
+        orow0 = (long long)bidx * args.M + row0;
+      }
+      const int col_base = nb * BN + half * HALF;
+      if (EPI == MOE_EPI_DGELU && lane == 0 && col_base < args.N) {
+        mbar_arrive_expect_tx(&ab[0], STG);
+        tma_load_2d(auxb, &tmAux, &ab[0], col_base, (int)orow0);
+      }
+      int32_t gidx[2] = {-1, -1};
+      if (EPI == MOE_EPI_GATHER_ADD && lane < nvalid) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          if (i < args.gk) gidx[i] = args.gidx[(orow0 + lane) * args.gk + i];
+      }
+      const bool has_k = num_kblocks(g) > 0;
       const uint32_t acc = tcount & 1;
       mbar_wait(&tfull[acc], (tcount >> 1) & 1);
       tc_fence_after();
-      const bool has_k = num_kblocks(g) > 0;
-      int m = mb * BM + r;
-      bool row_ok;
-      long long out_row;
-      int bidx;
-      if (KIND == 0) {
-        row_ok = m < args.gm[g];
-        out_row = (long long)args.gc[g] + m;
-        bidx = args.gb[g];
-      } else {
-        row_ok = m < args.M;
-        bidx = args.gb[tab[g]];
-        out_row = (long long)bidx * args.M + m;
-      }
-      const uint32_t t_row = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+      const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * HALF;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < NCH; ++c) {
         __syncwarp();
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_row + c * 32, v);
-        tmem_ld_wait();
-        const int n0 = nb * BN + c * 32;
-        if (!row_ok || n0 >= args.N) continue;
-        float f[32];
+        float f[CW];
+        {
+          uint32_t v[CW];
+          if constexpr (CW == 32) tmem_ld_32x32b_x32(t_row + c * CW, v);
+          else tmem_ld_32x32b_x16(t_row + c * CW, v);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.0f;
-        const bool full_cols = n0 + 32 <= args.N;
-        if (args.bias != nullptr && EPI != MOE_EPI_ATOMIC_ADD && EPI != MOE_EPI_DGELU) {
-          const float* bp = args.bias + (long long)bidx * args.N + n0;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] += (full_cols || n0 + i < args.N) ? bp[i] : 0.0f;
+          for (int i = 0; i < CW; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.0f;
         }
+        const int n0 = col_base + c * CW;
+        if (EPI == MOE_EPI_DGELU && lane == 0 && c + 1 < NCH && n0 + CW < args.N) {
+          mbar_arrive_expect_tx(&ab[(c + 1) & 1], STG);
+          tma_load_2d(auxb + ((c + 1) & 1) * STG, &tmAux, &ab[(c + 1) & 1], n0 + CW, (int)orow0);
+        }
+        if (n0 >= args.N) continue;
+        if (EPI == MOE_EPI_DGELU) {
+          mbar_wait(&ab[c & 1], aph[c & 1]);
+          aph[c & 1] ^= 1;
+        }
+        if (nvalid == 0) continue;
+        const int ncols = min(CW, args.N - n0);
+        const bool full_tile = nvalid == 32 && ncols == CW;
+        const bool row_ok = lane < nvalid;
         if (EPI == MOE_EPI_ATOMIC_ADD) {
-          float* Cp = reinterpret_cast<float*>(args.C);
-          for (int i = 0; i < 32; ++i) {
-            const int n = n0 + i;
-            if (n >= args.N) break;
-            const long long idx = args.transpose_c
-                                      ? (long long)n * args.ldc + out_row
-                                      : out_row * args.ldc + n;
-            atomicAdd(Cp + idx, f[i]);
+          if (row_ok) {
+            float* Cp = reinterpret_cast<float*>(args.C);
+            const long long m = orow0 + lane;
+#pragma unroll
+            for (int i = 0; i < CW; ++i) {
+              if (i >= ncols) continue;
+              const long long idx = args.transpose_c ? (long long)(n0 + i) * args.ldc + m
+                                                     : m * args.ldc + n0 + i;
+              atomicAdd(Cp + idx, f[i]);
+            }
           }
           continue;
         }
-        if (EPI == MOE_EPI_DGELU) {
-          const __nv_bfloat16* hp = args.aux + out_row * args.ldc + n0;
-          if (full_cols) {
+        if (args.bias != nullptr && EPI != MOE_EPI_DGELU && EPI != MOE_EPI_GATHER_ADD) {
+          const float* bp = args.bias + (long long)bidx * args.N + n0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 hv = *reinterpret_cast<const uint4*>(hp + q * 8);
+          for (int i = 0; i < CW; ++i) f[i] += (i < ncols) ? bp[i] : 0.0f;
+        }
+        float f2[CW];
+        if (EPI == MOE_EPI_GELU) {
+#pragma unroll
+          for (int i = 0; i < CW; ++i) {
+            const float h = f[i];
+            const float e = erff(h * 0.70710678118654752440f);
+            f[i] = 0.5f * h * (1.0f + e);
+            f2[i] = 0.5f * (1.0f + e) + h * 0.39894228040143267794f * __expf(-0.5f * h * h);
+          }
+        }
+        if (EPI == MOE_EPI_DGELU) {
+          const uint8_t* ax = auxb + (c & 1) * STG;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint4 hv = *reinterpret_cast<const uint4*>(ax + sw64(lane, j));
+            const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&hv);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[j * 8 + i] *= bf2f(h8[i]);
+          }
+        }
+        if (EPI == MOE_EPI_GATHER_ADD) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            if (i >= args.gk || gidx[i] < 0) continue;
+            const __nv_bfloat16* src =
+                reinterpret_cast<const __nv_bfloat16*>(args.gsrc) + (long long)gidx[i] * args.N + n0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint4 hv = *reinterpret_cast<const uint4*>(src + j * 8);
               const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&hv);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) f[q * 8 + i] *= gelu_grad_f(bf2f(h8[i]));
+              for (int u = 0; u < 8; ++u) f[j * 8 + u] += bf2f(h8[u]);
             }
-          } else {
-            for (int i = 0; i < 32; ++i)
-              if (n0 + i < args.N) f[i] *= gelu_grad_f(bf2f(hp[i]));
           }
         }
-        if (EPI == MOE_EPI_GELU) {
-          __nv_bfloat16* c2 = reinterpret_cast<__nv_bfloat16*>(args.C2) + out_row * args.ldc + n0;
-          if (full_cols) {
+        const bool want_colsum = EPI == MOE_EPI_DGELU && args.colsum != nullptr;
+        if (full_tile || want_colsum) {
+          if (lane == 0) bulk_wait_read0();  // previous store out of this buffer is done
+          __syncwarp();
+          if (!row_ok) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 o;
-              o.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
-              o.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
-              o.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
-              o.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
-              *reinterpret_cast<uint4*>(c2 + q * 8) = o;
-            }
-          } else {
-            for (int i = 0; i < 32; ++i)
-              if (n0 + i < args.N) c2[i] = f2bf(f[i]);
+            for (int i = 0; i < CW; ++i) f[i] = 0.0f;
           }
-#pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = gelu_f(f[i]);
+          stage_row<CF32>(stg, lane, f);
+          if (EPI == MOE_EPI_GELU) stage_row<CF32>(stg2, lane, f2);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (full_tile && lane == 0) {
+            tma_store_2d(&tmC, stg, n0, (int)orow0);
+            if (EPI == MOE_EPI_GELU) tma_store_2d(&tmC2, stg2, n0, (int)orow0);
+            bulk_commit();
+          }
         }
-        if (CF32) {
-          float* cp = reinterpret_cast<float*>(args.C) + out_row * args.ldc + n0;
-          if (full_cols) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              *reinterpret_cast<float4*>(cp + q * 4) =
-                  make_float4(f[q * 4], f[q * 4 + 1], f[q * 4 + 2], f[q * 4 + 3]);
-          } else {
-            for (int i = 0; i < 32; ++i)
-              if (n0 + i < args.N) cp[i] = f[i];
-          }
-        } else {
-          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(args.C) + out_row * args.ldc + n0;
-          if (full_cols) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 o;
-              o.x = pack_bf16x2(f[q * 8 + 0], f[q * 8 + 1]);
-              o.y = pack_bf16x2(f[q * 8 + 2], f[q * 8 + 3]);
-              o.z = pack_bf16x2(f[q * 8 + 4], f[q * 8 + 5]);
-              o.w = pack_bf16x2(f[q * 8 + 6], f[q * 8 + 7]);
-              *reinterpret_cast<uint4*>(cp + q * 8) = o;
-            }
-          } else {
-            for (int i = 0; i < 32; ++i)
-              if (n0 + i < args.N) cp[i] = f2bf(f[i]);
+        if (!full_tile && row_ok) {
+          const long long off = (orow0 + lane) * args.ldc + n0;
+          store_row_direct<CF32>(args.C, off, ncols, f);
+          if (EPI == MOE_EPI_GELU) store_row_direct<CF32>(args.C2, off, ncols, f2);
+        }
+        if (want_colsum && !CF32) {
+          // column sums of the stored (bf16-rounded) values, rows >= nvalid are zero
+          if (lane < ncols) {
+            float s = 0.f;
+            const uint32_t j = lane >> 3, e = lane & 7;
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r)
+              s += bf2f(*reinterpret_cast<const __nv_bfloat16*>(stg + sw64(r, j) + e * 2));
+            atomicAdd(args.colsum + (long long)bidx * args.N + n0 + lane, s);
           }
         }
       }
@@ -399,6 +504,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (lane == 0) bulk_wait0();
   }
 
   __syncthreads();
@@ -429,38 +535,39 @@ static EncodeFn encode_fn() {
   return fn;
 }
 
-// bf16 2D map over a row-major [outer][inner] matrix with row stride `ld`
-// elements, 128B swizzle, zero OOB fill.
+// 2D map over a row-major [outer][inner] matrix with row stride `ld` elements.
 static CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint64_t ld,
-                            uint32_t box_inner, uint32_t box_outer) {
+                            uint32_t box_inner, uint32_t box_outer, bool f32 = false,
+                            CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
-  const cuuint64_t dims[2] = {inner, outer};
-  const cuuint64_t strides[1] = {ld * 2};
+  const uint64_t es = f32 ? 4 : 2;
+  const cuuint64_t dims[2] = {inner, outer ? outer : 1};
+  const cuuint64_t strides[1] = {ld * es};
   const cuuint32_t box[2] = {box_inner, box_outer};
-  const cuuint32_t es[2] = {1, 1};
+  const cuuint32_t estr[2] = {1, 1};
   require((reinterpret_cast<uintptr_t>(base) & 15) == 0, MOE_ERR_INVALID_ARGUMENT,
           "gemm: operand base must be 16-byte aligned");
-  require((ld * 2) % 16 == 0, MOE_ERR_INVALID_ARGUMENT,
+  require((ld * es) % 16 == 0, MOE_ERR_INVALID_ARGUMENT,
           "gemm: operand row stride must be a multiple of 16 bytes");
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
-                                 dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  require(r == CUDA_SUCCESS, MOE_ERR_CUDA, "tma: cuTensorMapEncodeTiled failed (" +
-                                               std::to_string((int)r) + ")");
+  const CUresult r = encode_fn()(
+      &m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+      const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, MOE_ERR_CUDA,
+          "tma: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
 }
 
 template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32>
 static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
-  using C_ = Cfg<BN>;
+  using C_ = Cfg<BN, EPI, CF32>;
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN, KIND, EPI, CF32>;
   static bool attr = false;
   if (!attr) {
     MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
     attr = true;
   }
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tcm, tc2, tax;
   if (KIND == 0) {
     const uint64_t lda = p.lda ? p.lda : p.K;
     ta = make_map(p.A, p.K, p.a_rows, lda, 64, BM);
@@ -479,6 +586,15 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
     ta = make_map(p.A, p.M, p.a_rows, lda, 64, 64);
     tb = make_map(p.B, p.N, p.b_rows ? p.b_rows : p.a_rows, ldb, 64, 64);
   }
+  const uint64_t c_rows = p.c_rows ? p.c_rows : (KIND == 0 ? p.a_rows : (uint64_t)p.num_b * p.M);
+  tcm = tc2 = tax = ta;
+  if (EPI != MOE_EPI_ATOMIC_ADD) {
+    tcm = make_map(p.C, p.N, c_rows, p.ldc, C_::CW, 32, CF32, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (EPI == MOE_EPI_GELU)
+      tc2 = make_map(p.C2, p.N, c_rows, p.ldc, C_::CW, 32, CF32, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (EPI == MOE_EPI_DGELU)
+      tax = make_map(p.aux, p.N, c_rows, p.ldc, 32, 32, false, CU_TENSOR_MAP_SWIZZLE_64B);
+  }
   Args a;
   a.groups = (int)p.groups;
   a.M = (int)p.M;
@@ -490,13 +606,16 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
   a.gb = p.b;
   a.C = p.C;
   a.C2 = p.C2;
-  a.aux = reinterpret_cast<const __nv_bfloat16*>(p.aux);
   a.bias = p.bias;
+  a.colsum = p.colsum;
+  a.gsrc = p.gather_src;
+  a.gidx = p.gather_idx;
+  a.gk = (int)p.gather_k;
   a.ldc = (long long)p.ldc;
   a.transpose_c = p.transpose_c;
   a.num_b = (int)p.num_b;
   const int grid = num_sms();
-  kern<<<grid, THREADS, C_::SMEM, st>>>(ta, tb, a);
+  kern<<<grid, THREADS, C_::SMEM, st>>>(ta, tb, tcm, tc2, tax, a);
   MOE_LAUNCH_CHECK("tc_gemm_kernel");
   count_launch();
 }
@@ -507,11 +626,11 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
   using namespace tc;
   arg_check(p.groups >= 1 && p.groups <= MAX_GROUPS, "gemm.groups: must be in [1, 1024]");
   arg_check(p.dtype_ab == MOE_DTYPE_BF16, "gemm.dtype_ab: tcgen05 path needs bf16");
+  const bool f32 = p.dtype_c == MOE_DTYPE_F32;
   if (p.kind == MOE_GEMM_RAGGED_M) {
     arg_check(p.K % BK == 0, "gemm.K: must be a multiple of 64");
     arg_check(p.N % 8 == 0, "gemm.N: must be a multiple of 8");
     arg_check(!p.transpose_c, "gemm.transpose_c: only for RAGGED_K atomic");
-    const bool f32 = p.dtype_c == MOE_DTYPE_F32;
     const bool bmn = p.b_mn_major != 0;
     if (p.N <= 64 && !bmn && p.epilogue == MOE_EPI_STORE) {
       if (f32) launch<64, false, false, 0, MOE_EPI_STORE, true>(p, st);
@@ -536,13 +655,19 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
         arg_check(bmn && !f32, "gemm.epilogue: DGELU needs MN-major B and bf16 C");
         launch<256, false, true, 0, MOE_EPI_DGELU, false>(p, st);
         return;
+      case MOE_EPI_GATHER_ADD:
+        arg_check(bmn && !f32 && p.gather_src && p.gather_idx && p.gather_k >= 1 &&
+                      p.gather_k <= 2,
+                  "gemm.epilogue: GATHER_ADD needs MN-major B, bf16 C, gather_src/idx, k<=2");
+        launch<256, false, true, 0, MOE_EPI_GATHER_ADD, false>(p, st);
+        return;
       default:
         fail(MOE_ERR_INVALID_ARGUMENT, "gemm.epilogue: unsupported for RAGGED_M");
     }
   } else {
     arg_check(p.M % BM == 0, "gemm.M: RAGGED_K needs M a multiple of 128");
     arg_check(p.N % 8 == 0, "gemm.N: must be a multiple of 8");
-    arg_check(p.dtype_c == MOE_DTYPE_F32, "gemm.dtype_c: RAGGED_K writes fp32");
+    arg_check(f32, "gemm.dtype_c: RAGGED_K writes fp32");
     if (p.epilogue == MOE_EPI_ATOMIC_ADD) {
       if (p.N <= 64) launch<64, true, true, 1, MOE_EPI_ATOMIC_ADD, true>(p, st);
       else launch<256, true, true, 1, MOE_EPI_ATOMIC_ADD, true>(p, st);

@@ -118,7 +118,7 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   gmk = dalloc<int32_t>(owned, E);
   gak = dalloc<int32_t>(owned, E);
   gbk = dalloc<int32_t>(owned, E);
-  H = dalloc_bytes(owned, rows * dff * esz);
+  Gp = dalloc_bytes(owned, rows * dff * esz);
   Aact = dalloc_bytes(owned, rows * dff * esz);
   Yl = dalloc_bytes(owned, slot_bytes);
   Yh = P > 1 ? dalloc_bytes(owned, slot_bytes) : Yl;
@@ -131,12 +131,11 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   dXh = P > 1 ? dalloc_bytes(owned, slot_bytes) : dXl;
   if (dt == MOE_DTYPE_BF16) dl_lp = dalloc_bytes(owned, T * Epad * 2);
   else dl_f32 = dalloc<float>(owned, T * E);
-  dxg = dalloc<float>(owned, T * dm);
   // Every row of the activation buffers holds finite values from here on, so
   // zero pad rows of the partner operand annihilate them in the RAGGED_K GEMMs.
   MOE_CUDA(cudaMemset(xs, 0, slot_bytes));
   if (xr != xs) MOE_CUDA(cudaMemset(xr, 0, slot_bytes));
-  MOE_CUDA(cudaMemset(H, 0, rows * dff * esz));
+  MOE_CUDA(cudaMemset(Gp, 0, rows * dff * esz));
   MOE_CUDA(cudaMemset(Aact, 0, rows * dff * esz));
   MOE_CUDA(cudaMemset(dH, 0, rows * dff * esz));
   MOE_CUDA(cudaMemset(dYs, 0, slot_bytes));
@@ -257,7 +256,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     p.A = xr;
     p.B = w.w1;
     p.C = Aact;
-    p.C2 = H;
+    p.C2 = Gp;
     p.bias = w.b1;
     p.ldc = dff;
     grouped_gemm(p, st);
@@ -318,7 +317,9 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   mark("route_bwd", st);
   if (P > 1) a2a(dYs, dYr, El * Cs * dm * esz, st);
   mark("a2a_dy", st);
-  // K5^T dgrad: dH = (dY W2) * gelu'(H); dXe = dH W1
+  // K5^T dgrad: dH = (dY W2) * gelu'(h) (stored by ffn1), db1 = column sums
+  // of dH fused into the same epilogue; dXe = dH W1
+  MOE_CUDA(cudaMemsetAsync(g.db1, 0, (uint64_t)El * dff * 4, st));
   {
     moe_gemm_problem_t p = expert_problem();
     p.epilogue = MOE_EPI_DGELU;
@@ -328,7 +329,8 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.A = dYr;
     p.B = w.w2;
     p.C = dH;
-    p.aux = H;
+    p.aux = Gp;
+    p.colsum = g.db1;
     p.ldc = dff;
     grouped_gemm(p, st);
   }
@@ -379,17 +381,17 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
     mark("wgrad_w2", st);
   }
-  group_colsum(P * El, gm, ga, gb, El, dff, dt, dH, g.db1, st, Cs);
   group_colsum(P * El, gm, ga, gb, El, dm, dt, dYr, g.db2, st, Cs);
   mark("bias_grads", st);
-  // gate: dx_gate = dlogits wg ; dwg = dlogits^T x (split-K, fp32 atomics)
+  // gate dgrad with the combine backward folded into its epilogue:
+  // dx[t] = dlogits[t] wg + sum_i dXe[slot_i]; dwg = dlogits^T x (split-K)
   if (T) {
     moe_gemm_problem_t p;
     std::memset(&p, 0, sizeof(p));
     p.kind = MOE_GEMM_RAGGED_M;
-    p.epilogue = MOE_EPI_STORE;
+    p.epilogue = MOE_EPI_GATHER_ADD;
     p.dtype_ab = dt;
-    p.dtype_c = MOE_DTYPE_F32;
+    p.dtype_c = dt;
     p.b_mn_major = 1;
     p.groups = 1;
     p.N = dm;
@@ -403,11 +405,14 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.b = gate_tab + 3;
     p.A = dt == MOE_DTYPE_BF16 ? dl_lp : (const void*)dl_f32;
     p.B = w.wg;
-    p.C = dxg;
+    p.C = dx;
     p.ldc = dm;
+    p.gather_src = dXh;
+    p.gather_idx = slot;
+    p.gather_k = k;
     grouped_gemm(p, st);
   }
-  mark("gate_dgrad", st);
+  mark("gate_dgrad_gather_dx", st);
   MOE_CUDA(cudaMemsetAsync(g.dwg, 0, (uint64_t)E * dm * 4, st));
   if (T) {
     moe_gemm_problem_t p;
@@ -434,8 +439,6 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("gate_wgrad", st);
-  gather_dx(T, dm, k, dt, dXh, slot, dxg, dx, st);
-  mark("gather_dx", st);
   if (P > 1) {
     MOE_NCCL(ncclGroupStart());
     MOE_NCCL(ncclAllReduce(g.dwg, g.dwg, (uint64_t)E * dm, ncclFloat32, ncclSum, (ncclComm_t)comm, st));

@@ -55,13 +55,12 @@ struct Layer {
   int32_t* cnt_recv = nullptr;
   int32_t *gm = nullptr, *ga = nullptr, *gb = nullptr, *gmk = nullptr, *gak = nullptr,
           *gbk = nullptr;
-  void *H = nullptr, *Aact = nullptr, *Yl = nullptr, *Yh = nullptr;
+  void *Gp = nullptr, *Aact = nullptr, *Yl = nullptr, *Yh = nullptr;
   // backward buffers
   float* dgate = nullptr;
   void *dYs = nullptr, *dYr = nullptr, *dH = nullptr, *dXl = nullptr, *dXh = nullptr;
   float* dl_f32 = nullptr;
   void* dl_lp = nullptr;
-  float* dxg = nullptr;
   // gate GEMM tables
   int32_t* gate_tab = nullptr;
   int32_t *split_m = nullptr, *split_a = nullptr, *split_b = nullptr;

@@ -30,7 +30,7 @@ def i32(v):
 
 
 def ragged_m_case(dtype, b_mn, epi, N=512, K=256, groups=(200, 0, 128, 37, 300), bvec=(0, 1, 2, 1, 0),
-                  Cs=320, bias=True, out_f32=False):
+                  Cs=320, bias=True, out_f32=False, colsum=False, gather=None):
     torch.manual_seed(0)
     G = len(groups)
     nb = max(bvec) + 1
@@ -58,6 +58,12 @@ def ragged_m_case(dtype, b_mn, epi, N=512, K=256, groups=(200, 0, 128, 37, 300),
     p.aux = aux.data_ptr()
     p.bias = bias_t.data_ptr() if bias_t is not None else None
     p.ldc = N
+    cs = torch.zeros(nb, N, device=dev) if colsum else None
+    if colsum:
+        p.colsum = cs.data_ptr()
+    if gather is not None:
+        gsrc, gidx, gk = gather
+        p.gather_src, p.gather_idx, p.gather_k = gsrc.data_ptr(), gidx.data_ptr(), gk
     grouped_gemm(p)
     torch.cuda.synchronize()
     # reference
@@ -69,13 +75,25 @@ def ragged_m_case(dtype, b_mn, epi, N=512, K=256, groups=(200, 0, 128, 37, 300),
             continue
         acc = A[r0:r0 + mm].float() @ Bmat[bvec[g]].float().t()
         if epi == _lib.MOE_EPI_DGELU:
-            acc = acc * gelu_grad(aux[r0:r0 + mm].float())
+            acc = acc * aux[r0:r0 + mm].float()
+        elif epi == _lib.MOE_EPI_GATHER_ADD:
+            gsrc, gidx, gk = gather
+            for i in range(gk):
+                ix = gidx[r0:r0 + mm, i].long()
+                ok = ix >= 0
+                acc[ok] += gsrc[ix[ok]].float()
         elif bias_t is not None:
             acc = acc + bias_t[bvec[g]]
         if epi == _lib.MOE_EPI_GELU:
-            refC2[r0:r0 + mm] = acc
+            refC2[r0:r0 + mm] = gelu_grad(acc)
             acc = gelu(acc)
         refC[r0:r0 + mm] = acc
+    if colsum:
+        ref_cs = torch.zeros(nb, N, device=dev)
+        for g in range(G):
+            r0, mm = g * Cs, groups[g]
+            ref_cs[bvec[g]] += Cm[r0:r0 + mm].float().sum(0)  # sums of the stored values
+        return Cm.float(), refC, cs, ref_cs
     return Cm.float(), refC, C2.float(), refC2
 
 
@@ -99,9 +117,37 @@ def test_tc_ragged_m_gelu():
     assert_close(got2, ref2, 1e-2)
 
 
-def test_tc_ragged_m_dgelu():
-    got, ref, _, _ = ragged_m_case(torch.bfloat16, True, _lib.MOE_EPI_DGELU, bias=False)
+def test_tc_ragged_m_dgelu_with_colsum():
+    got, ref, cs, ref_cs = ragged_m_case(torch.bfloat16, True, _lib.MOE_EPI_DGELU, bias=False,
+                                         colsum=True)
     assert_close(got, ref, 1e-2)
+    assert_close(cs, ref_cs, 1e-4)
+
+
+def test_tc_gather_add():
+    torch.manual_seed(3)
+    T, N, K, k = 1000, 512, 64, 2
+    gsrc = (torch.rand(3000, N, device=dev) * 2 - 1).to(torch.bfloat16)
+    gidx = torch.randint(-1, 3000, (T, k), device=dev, dtype=torch.int32)
+    got, ref, _, _ = ragged_m_case(torch.bfloat16, True, _lib.MOE_EPI_GATHER_ADD, N=N, K=K,
+                                   groups=(T,), bvec=(0,), Cs=T, bias=False,
+                                   gather=(gsrc, gidx, k))
+    assert_close(got, ref, 1e-2)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32])
+def test_simt_gather_add_and_colsum(dtype):
+    torch.manual_seed(4)
+    T, N, K, k = 300, 96, 32, 2
+    gsrc = torch.rand(500, N, device=dev) * 2 - 1
+    gidx = torch.randint(-1, 500, (T, k), device=dev, dtype=torch.int32)
+    got, ref, _, _ = ragged_m_case(dtype, True, _lib.MOE_EPI_GATHER_ADD, N=N, K=K, groups=(T,),
+                                   bvec=(0,), Cs=T, bias=False, gather=(gsrc, gidx, k))
+    assert_close(got, ref, 2e-6)
+    got, ref, cs, ref_cs = ragged_m_case(dtype, True, _lib.MOE_EPI_DGELU, N=N, K=K, bias=False,
+                                         colsum=True)
+    assert_close(got, ref, 2e-6)
+    assert_close(cs, ref_cs, 2e-6)
 
 
 def test_tc_small_n_masked():
