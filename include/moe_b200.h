@@ -53,6 +53,9 @@ const char* moe_last_error(void);
 int moe_abi_version(void);
 /* Number of kernels this library launched since load (all entry points). */
 uint64_t moe_kernel_launch_count(void);
+/* sizeof() of an ABI struct by type name ("moe_gemm_problem_t", ...), 0 if
+ * unknown — lets FFI bindings verify their struct layouts at load time. */
+uint64_t moe_abi_sizeof(const char* type_name);
 
 /* ======================================================================
  * 1. moesim compatibility layer (host buffers, device execution)

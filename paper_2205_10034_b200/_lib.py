@@ -108,6 +108,11 @@ class GemmProblem(C.Structure):
         ("lda", C.c_uint64),
         ("ldb", C.c_uint64),
         ("b_rows", C.c_uint64),
+        ("c_rows", C.c_uint64),
+        ("colsum", C.c_void_p),
+        ("gather_src", C.c_void_p),
+        ("gather_idx", C.c_void_p),
+        ("gather_k", C.c_uint32),
     ]
 
 
@@ -166,6 +171,7 @@ SIGNATURES = {
     "moe_last_error": (C.c_char_p, []),
     "moe_abi_version": (C.c_int, []),
     "moe_kernel_launch_count": (_U64, []),
+    "moe_abi_sizeof": (_U64, [C.c_char_p]),
     "moesim_alltoall_flat": (_I, [_U64, _U64, _VP, _VP, _VP, _VP]),
     "moesim_fuse_slices": (_I, [_U64, _VP, _VP, _VP, _VP]),
     "moesim_split_blob": (_I, [_U64, _VP, _U64, _VP, _VP]),
@@ -218,6 +224,18 @@ def _load():
 
 
 lib = _load()
+
+STRUCTS = {
+    "moe_slice_index_entry_t": SliceIndexEntry, "moe_routing_out_t": RoutingOut,
+    "moe_gemm_problem_t": GemmProblem, "moe_layer_desc_t": LayerDesc,
+    "moe_layer_params_t": LayerParams, "moe_layer_grads_t": LayerGrads,
+    "moe_ring_desc_t": RingDesc, "moe_ring_timeline_t": RingTimeline,
+}
+for _n, _t in STRUCTS.items():  # layouts must match include/moe_b200.h exactly
+    _sz = lib.moe_abi_sizeof(_n.encode())
+    if _sz != C.sizeof(_t):
+        raise ImportError(f"ABI mismatch: {_n} is {_sz} bytes in the library, "
+                          f"{C.sizeof(_t)} in the Python binding")
 
 
 def check(status: int) -> None:

@@ -63,6 +63,20 @@ const char* moe_last_error(void) { return g_last_error.c_str(); }
 int moe_abi_version(void) { return MOE_ABI_VERSION; }
 uint64_t moe_kernel_launch_count(void) { return moe::g_launches.load(); }
 
+uint64_t moe_abi_sizeof(const char* n) {
+  if (!n) return 0;
+  const std::string s(n);
+  if (s == "moe_slice_index_entry_t") return sizeof(moe_slice_index_entry_t);
+  if (s == "moe_routing_out_t") return sizeof(moe_routing_out_t);
+  if (s == "moe_gemm_problem_t") return sizeof(moe_gemm_problem_t);
+  if (s == "moe_layer_desc_t") return sizeof(moe_layer_desc_t);
+  if (s == "moe_layer_params_t") return sizeof(moe_layer_params_t);
+  if (s == "moe_layer_grads_t") return sizeof(moe_layer_grads_t);
+  if (s == "moe_ring_desc_t") return sizeof(moe_ring_desc_t);
+  if (s == "moe_ring_timeline_t") return sizeof(moe_ring_timeline_t);
+  return 0;
+}
+
 // ------------------------------------------------------- moesim compat ----
 moe_status_t moesim_alltoall_flat(uint64_t ranks, uint64_t n_chunks, const uint64_t* lens,
                                   const uint8_t* data, uint64_t* out_lens, uint8_t* out_data) {
