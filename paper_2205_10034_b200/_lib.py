@@ -35,6 +35,7 @@ MOE_EPI_STORE = 0
 MOE_EPI_GELU = 1
 MOE_EPI_DGELU = 2
 MOE_EPI_ATOMIC_ADD = 3
+MOE_EPI_GATHER_ADD = 4
 
 
 class ConfigError(RuntimeError):

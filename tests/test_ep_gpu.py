@@ -1,0 +1,120 @@
+"""GPU x2+: expert parallelism over NCCL (K4).  Each rank holds E/P experts and
+T tokens; the EP layer must reproduce, per rank, the single-GPU layer that holds
+all E experts on the same tokens: y and dx bit-identical (rows are computed by
+the same tiles in the same K order), expert weight gradients equal to the sum
+of the per-rank single-GPU gradients, gate gradients all-reduced.  Also the
+packed all-to-all itself (fused = 1 message per peer vs unfused slices) against
+alltoall_flat semantics (collectives.cpp:10-21)."""
+import os
+import socket
+
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+    pytest.skip("needs >= 2 GPUs", allow_module_level=True)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, q):
+    try:
+        import torch.distributed as dist
+
+        from paper_2205_10034_b200 import EPGroup, MoEConfig, MoELayer
+        from paper_2205_10034_b200.layer import T_DY
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world, device_id=torch.device("cuda", rank))
+        ep = EPGroup(world, rank)
+        if case == "a2a":
+            R = world
+            n = 3 * 4096 + 16  # bytes per peer, not a multiple of anything nice
+            send = torch.randint(0, 255, (R * n,), dtype=torch.uint8, device="cuda",
+                                 generator=torch.Generator("cuda").manual_seed(rank))
+            for fused, slices in ((True, 1), (False, 4)):
+                recv = torch.zeros_like(send)
+                nn = n if fused else n - n % slices
+                ep.alltoall_packed(send, recv, nn, slices_per_peer=slices, fused=fused)
+                torch.cuda.synchronize()
+                allsend = [torch.zeros_like(send) for _ in range(R)]
+                dist.all_gather(allsend, send)
+                for s in range(R):  # recv chunk s == sender s's chunk for me
+                    assert torch.equal(recv[s * nn:(s + 1) * nn], allsend[s][rank * n:rank * n + nn])
+            q.put((rank, "ok"))
+            return
+        E, k, d, dff, T, dt = case
+        cfg = MoEConfig(E, k, d, dff, 1.25, T, dt)
+        lep = MoELayer(cfg, ep=ep)
+        lep.init_params(99)
+        x = lep.make_input(99)
+        dy = lep.make_input(99, T_DY)
+        y = lep.forward(x)
+        dx = lep.backward(dy, d_aux=0.02)
+        # single-GPU layer with all experts, same tokens
+        l1 = MoELayer(cfg)
+        l1.init_params(99)
+        l1.rank = rank  # inputs of this rank
+        x1 = l1.make_input(99)
+        dy1 = l1.make_input(99, T_DY)
+        assert torch.equal(x, x1)
+        y1 = l1.forward(x1)
+        dx1 = l1.backward(dy1, d_aux=0.02)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y1), "EP forward differs from single-GPU"
+        assert torch.equal(dx, dx1), "EP dx differs from single-GPU"
+        El = E // world
+        g1 = {n: t.clone() for n, t in l1.grads.items()}
+        for n in g1:
+            dist.all_reduce(g1[n])  # sum over ranks of the single-GPU gradients
+        sl = slice(rank * El, (rank + 1) * El)
+        for n in ("dw1", "db1", "dw2", "db2"):
+            ref = g1[n][sl]
+            err = (lep.grads[n] - ref).abs().max() / ref.abs().max()
+            assert err < 2e-3, (n, err.item())
+        err = (lep.grads["dwg"] - g1["dwg"]).abs().max() / g1["dwg"].abs().max()
+        assert err < 1e-4, ("dwg", err.item())
+        lep.close()
+        ep.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # report to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+        raise
+
+
+def _run(case, world=2):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    for r, msg in res:
+        assert msg == "ok", f"rank {r}:\n{msg}"
+
+
+def test_packed_alltoall_fused_and_unfused():
+    _run("a2a")
+
+
+@pytest.mark.parametrize("case", [
+    (8, 2, 256, 512, 1024, torch.bfloat16),
+    (64, 1, 1024, 4096, 8192, torch.bfloat16),
+    (8, 2, 128, 256, 512, torch.float32),
+])
+def test_ep_layer_matches_single_gpu(case):
+    _run(case, world=min(torch.cuda.device_count(), 2))
