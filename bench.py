@@ -190,7 +190,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=0, help="override T (tokens per GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--phases", action="store_true", help="print a per-phase breakdown line")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="EP token exchange for N>1: NVLink peer stores (p2p) or NCCL all-to-all")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
@@ -215,7 +216,8 @@ def main():
         ep = EPGroup(ws, rank)
     dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     E, k, d, dff, T, cf = cfg["E"], cfg["k"], cfg["d"], cfg["dff"], cfg["T"], cfg["cf"]
-    mcfg = MoEConfig(E, k, d, dff, cf, T, dtype, gate_bias=bool(cfg.get("skew")))
+    mcfg = MoEConfig(E, k, d, dff, cf, T, dtype, gate_bias=bool(cfg.get("skew")),
+                     exchange=args.exchange)
     layer = MoELayer(mcfg, ep=ep, device=dev)
     gb = None
     if cfg.get("skew"):
@@ -350,6 +352,7 @@ def main():
                    "d_model": d, "d_ff": dff, "capacity_factor": cf,
                    "capacity": layer.capacity, "experts_per_gpu": E // ws,
                    "parallelism": f"ep{ws}" if ws > 1 else "single",
+                   "exchange": args.exchange if ws > 1 else None,
                    "l2": "inputs larger than L2 (x 128 MiB + weights 1 GiB per step), no flush"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks,

@@ -224,7 +224,17 @@ typedef struct moe_layer_desc {
   uint32_t ep_size;        /* P ranks; E % P == 0 */
   uint32_t ep_rank;
   void* nccl_comm;         /* ncclComm_t when ep_size > 1 (see moe_comm_*) */
+  uint32_t exchange;       /* ep_size > 1: MOE_EXCHANGE_P2P (default) or MOE_EXCHANGE_NCCL */
 } moe_layer_desc_t;
+
+/* EP token exchange.  P2P: the dispatch / combine-backward kernels store rows
+ * straight into the peers' receive buffers over NVLink (CUDA IPC mappings,
+ * exact row counts, no capacity padding on the wire) and expert outputs are
+ * pushed back the same way; device-side epoch flags order producers and
+ * consumers (no host synchronisation).  NCCL: capacity-padded ncclAlltoAll of
+ * the packed buffers (the baseline lowering). */
+#define MOE_EXCHANGE_P2P 0
+#define MOE_EXCHANGE_NCCL 1
 
 typedef struct moe_layer* moe_layer_t;
 

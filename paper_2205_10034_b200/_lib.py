@@ -130,6 +130,7 @@ class LayerDesc(C.Structure):
         ("ep_size", C.c_uint32),
         ("ep_rank", C.c_uint32),
         ("nccl_comm", C.c_void_p),
+        ("exchange", C.c_uint32),
     ]
 
 

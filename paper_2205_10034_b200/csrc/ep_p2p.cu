@@ -1,0 +1,400 @@
+// K4 over NVLink peer memory: the dispatch and combine-backward kernels store
+// token rows straight into the owning rank's receive buffer (CUDA IPC mapping
+// of one window per rank), and expert outputs are pushed back the same way —
+// the exchange is fused into the kernels that produce the rows, moves exactly
+// the kept rows (no capacity padding on the wire) and needs no host sync.
+//
+// Ordering: every producing kernel ends with a grid-wide "last block" step that
+// publishes `epoch` into each destination's flags[slot][me] with a
+// system-scope release store after all its remote stores are fenced
+// (fence.sc.sys per thread, then an atomic ticket); consumers spin on
+// ld.acquire.sys in a one-block wait kernel.  Reuse safety: a phase (forward or
+// backward) starts only after every peer has finished its previous phase
+// (SLOT_PHASE), which is when it last read the buffers this phase overwrites.
+// Spins time out after 30 s with __trap() rather than hanging the device.
+//
+// Layout and receive order follow alltoall_flat (collectives.cpp:10-21): rank
+// r's receive buffer is [src][local expert][Cs][d], i.e. sources in rank order.
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "common.cuh"
+#include "ep_p2p.h"
+#include "kernels.h"
+
+namespace moe {
+
+namespace {
+
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct Win {
+  uint8_t** peers;
+  uint64_t off_flags;
+  uint32_t P, me;
+};
+
+__device__ __forceinline__ uint64_t* flag_at(uint8_t* base, uint64_t off_flags, uint32_t P,
+                                             int slot, uint32_t src) {
+  return reinterpret_cast<uint64_t*>(base + off_flags) + (uint64_t)slot * P + src;
+}
+
+// All threads of every block call this exactly once at the end of a producing
+// kernel; the last block to arrive publishes the epoch to every peer.
+__device__ void grid_done_signal(const Win& w, uint32_t* ctr, int slot, uint64_t value) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned prev = atomicAdd(ctr, 1u);
+    if (prev == nb - 1) {
+      __threadfence_system();
+      for (uint32_t p = 0; p < w.P; ++p)
+        if (p != w.me) st_release_sys(flag_at(w.peers[p], w.off_flags, w.P, slot, w.me), value);
+      atomicExch(ctr, 0u);
+    }
+  }
+}
+
+__global__ void p2p_wait_kernel(const uint64_t* flags, uint32_t P, uint32_t me, int slot,
+                                uint64_t target, int32_t* err) {
+  const uint32_t p = threadIdx.x;
+  if (p < P && p != me) {
+    const uint64_t* f = flags + (uint64_t)slot * P + p;
+    const uint64_t t0 = globaltimer();
+    while (ld_acquire_sys(f) < target) {
+      if (globaltimer() - t0 > 30000000000ull) {
+        atomicExch(err, 1000 + slot * 16 + (int)p);
+        __trap();
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void p2p_signal_kernel(Win w, int slot, uint64_t value) {
+  __threadfence_system();
+  const uint32_t p = threadIdx.x;
+  if (p < w.P && p != w.me) st_release_sys(flag_at(w.peers[p], w.off_flags, w.P, slot, w.me), value);
+}
+
+template <typename T>
+struct V8;  // elements per 16B vector
+template <>
+struct V8<__nv_bfloat16> {
+  static constexpr int N = 8;
+};
+template <>
+struct V8<float> {
+  static constexpr int N = 4;
+};
+
+// grid: [0, ntb) token blocks (8 warps, warp per token) + E expert blocks
+template <typename T>
+__global__ void __launch_bounds__(256) p2p_dispatch_kernel(
+    Win w, uint64_t off_xr, uint64_t off_cnt, uint32_t* ctr, uint64_t T_, int d, int E, int El,
+    int k, uint64_t C, uint64_t Cs, const T* __restrict__ x, const int32_t* __restrict__ expert,
+    const int32_t* __restrict__ position, const int32_t* __restrict__ kept,
+    int32_t* __restrict__ slot, uint64_t ntb, uint64_t epoch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nv = d / V8<T>::N;
+  if (blockIdx.x < ntb) {
+    const uint64_t t = blockIdx.x * 8ull + warp;
+    if (t < T_) {
+      uint4* dst[2] = {nullptr, nullptr};
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (i >= k) break;
+        const int e = expert[t * k + i];
+        const int p = position[t * k + i];
+        const bool keep = (uint64_t)p < C;
+        if (lane == 0) slot[t * k + i] = keep ? (int32_t)(e * Cs + p) : -1;
+        if (keep) {
+          const int r = e / El, j = e % El;
+          const uint64_t row = ((uint64_t)w.me * El + j) * Cs + p;
+          dst[i] = reinterpret_cast<uint4*>(w.peers[r] + off_xr + row * d * sizeof(T));
+        }
+      }
+      const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
+      for (int v = lane; v < nv; v += 32) {
+        const uint4 val = __ldg(src + v);
+        if (dst[0]) dst[0][v] = val;
+        if (dst[1]) dst[1][v] = val;
+      }
+    }
+  } else {
+    const int e = (int)(blockIdx.x - ntb);
+    const int r = e / El, j = e % El;
+    const int n = kept[e];
+    const uint64_t base_row = ((uint64_t)w.me * El + j) * Cs;
+    if (threadIdx.x == 0)
+      reinterpret_cast<int32_t*>(w.peers[r] + off_cnt)[w.me * El + j] = n;
+    const int end = (int)min((uint64_t)((n + 63) / 64) * 64, Cs);
+    for (int rr = n + warp; rr < end; rr += 8) {
+      uint4* row = reinterpret_cast<uint4*>(w.peers[r] + off_xr + (base_row + rr) * d * sizeof(T));
+      for (int v = lane; v < nv; v += 32) row[v] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  grid_done_signal(w, ctr, SLOT_DISPATCH, epoch);
+}
+
+template <typename T>
+__device__ __forceinline__ void ld8(const T* p, float (&f)[8]);
+template <>
+__device__ __forceinline__ void ld8<__nv_bfloat16>(const __nv_bfloat16* p, float (&f)[8]) {
+  const uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(h[i]);
+}
+template <>
+__device__ __forceinline__ void ld8<float>(const float* p, float (&f)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0];
+  const float4 b = reinterpret_cast<const float4*>(p)[1];
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+template <typename T>
+__device__ __forceinline__ void st8(T* p, const float (&f)[8]);
+template <>
+__device__ __forceinline__ void st8<__nv_bfloat16>(__nv_bfloat16* p, const float (&f)[8]) {
+  uint4 o;
+  o.x = pack_bf16x2(f[0], f[1]);
+  o.y = pack_bf16x2(f[2], f[3]);
+  o.z = pack_bf16x2(f[4], f[5]);
+  o.w = pack_bf16x2(f[6], f[7]);
+  *reinterpret_cast<uint4*>(p) = o;
+}
+template <>
+__device__ __forceinline__ void st8<float>(float* p, const float (&f)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(f[0], f[1], f[2], f[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(f[4], f[5], f[6], f[7]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) p2p_combine_bwd_kernel(
+    Win w, uint64_t off_dyr, uint64_t off_yh, uint32_t* ctr, uint64_t T_, int d, int E, int El,
+    int k, uint64_t C, uint64_t Cs, const T* __restrict__ dy, const int32_t* __restrict__ slot,
+    const float* __restrict__ gate, const int32_t* __restrict__ expert,
+    const int32_t* __restrict__ position, const int32_t* __restrict__ kept,
+    float* __restrict__ dgate, uint64_t ntb, uint64_t epoch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const T* Yh = reinterpret_cast<const T*>(w.peers[w.me] + off_yh);
+  if (blockIdx.x < ntb) {
+    const uint64_t t = blockIdx.x * 8ull + warp;
+    if (t < T_) {
+      for (int i = 0; i < k; ++i) {
+        const int32_t s = slot[t * k + i];
+        if (s < 0) {
+          if (lane == 0) dgate[t * k + i] = 0.f;
+          continue;
+        }
+        const int e = expert[t * k + i], p = position[t * k + i];
+        const int r = e / El, j = e % El;
+        T* dst = reinterpret_cast<T*>(w.peers[r] + off_dyr) +
+                 (((uint64_t)w.me * El + j) * Cs + p) * d;
+        const float g = gate[t * k + i];
+        float dot = 0.f;
+        for (int c = lane * 8; c < d; c += 256) {
+          float a[8], b[8], o[8];
+          ld8<T>(dy + t * d + c, a);
+          ld8<T>(Yh + (uint64_t)s * d + c, b);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            dot = fmaf(a[q], b[q], dot);
+            o[q] = g * a[q];
+          }
+          st8<T>(dst + c, o);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == 0) dgate[t * k + i] = dot;
+      }
+    }
+  } else {
+    const int e = (int)(blockIdx.x - ntb);
+    const int r = e / El, j = e % El;
+    const int n = kept[e];
+    const uint64_t base_row = ((uint64_t)w.me * El + j) * Cs;
+    const int end = (int)min((uint64_t)((n + 63) / 64) * 64, Cs);
+    const int nv = d / V8<T>::N;
+    for (int rr = n + warp; rr < end; rr += 8) {
+      uint4* row = reinterpret_cast<uint4*>(w.peers[r] + off_dyr + (base_row + rr) * d * sizeof(T));
+      for (int v = lane; v < nv; v += 32) row[v] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  grid_done_signal(w, ctr, SLOT_DY, epoch);
+}
+
+// grid (P*El groups, row chunks of 32); warp per row
+__global__ void __launch_bounds__(256) p2p_push_kernel(Win w, uint64_t home_off, uint64_t off_cnt,
+                                                       uint32_t* ctr, const uint8_t* __restrict__ src,
+                                                       int El, uint64_t Cs, uint64_t row_bytes,
+                                                       int slot_id, uint64_t epoch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x;
+  const int s = g / El, j = g % El;
+  const int cnt = reinterpret_cast<const int32_t*>(w.peers[w.me] + off_cnt)[g];
+  const int r0 = blockIdx.y * 32;
+  const uint64_t nv = row_bytes / 16;
+  for (int r = r0 + warp; r < min(cnt, r0 + 32); r += 8) {
+    const uint4* from = reinterpret_cast<const uint4*>(src + ((uint64_t)g * Cs + r) * row_bytes);
+    uint4* to = reinterpret_cast<uint4*>(w.peers[s] + home_off +
+                                         (((uint64_t)w.me * El + j) * Cs + r) * row_bytes);
+    for (uint64_t v = lane; v < nv; v += 32) to[v] = __ldg(from + v);
+  }
+  grid_done_signal(w, ctr, slot_id, epoch);
+}
+
+uint64_t a256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+Win win_of(const P2PWindow& w) { return Win{w.peer_dev, w.off_flags, w.P, w.me}; }
+uint32_t* ctr_of(const P2PWindow& w, int i) {
+  return reinterpret_cast<uint32_t*>(w.base + w.off_ctr) + i;
+}
+
+}  // namespace
+
+#define P2P_NCCL(expr)                                                                \
+  do {                                                                                \
+    ncclResult_t _r = (expr);                                                         \
+    if (_r != ncclSuccess)                                                            \
+      ::moe::fail(MOE_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));  \
+  } while (0)
+
+void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint64_t slice_bytes,
+               uint64_t home_bytes, uint32_t E, cudaStream_t st) {
+  config_check(P <= 8, "layer.ep_size: P2P exchange supports up to 8 GPUs of one box");
+  w.P = P;
+  w.me = me;
+  w.off_xr = 0;
+  w.off_dyr = a256(w.off_xr + slice_bytes);
+  w.off_yh = a256(w.off_dyr + slice_bytes);
+  w.off_dxh = a256(w.off_yh + home_bytes);
+  w.off_cnt = a256(w.off_dxh + home_bytes);
+  w.off_flags = a256(w.off_cnt + (uint64_t)E * 4);
+  w.off_ctr = a256(w.off_flags + (uint64_t)NSLOT * P * 8);
+  w.bytes = w.off_ctr + 256;
+  MOE_CUDA(cudaMalloc(&w.base, w.bytes));
+  MOE_CUDA(cudaMemsetAsync(w.base, 0, w.bytes, st));
+  MOE_CUDA(cudaMalloc(&w.err, sizeof(int32_t)));
+  MOE_CUDA(cudaMemsetAsync(w.err, 0, sizeof(int32_t), st));
+  cudaIpcMemHandle_t h;
+  MOE_CUDA(cudaIpcGetMemHandle(&h, w.base));
+  uint8_t* dh = nullptr;
+  MOE_CUDA(cudaMalloc(&dh, (uint64_t)P * sizeof(h)));
+  MOE_CUDA(cudaMemcpyAsync(dh + me * sizeof(h), &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  P2P_NCCL(ncclAllGather(dh + me * sizeof(h), dh, sizeof(h), ncclUint8, (ncclComm_t)nccl_comm, st));
+  std::vector<cudaIpcMemHandle_t> all(P);
+  MOE_CUDA(cudaMemcpyAsync(all.data(), dh, (uint64_t)P * sizeof(h), cudaMemcpyDeviceToHost, st));
+  MOE_CUDA(cudaStreamSynchronize(st));
+  MOE_CUDA(cudaFree(dh));
+  for (uint32_t p = 0; p < P; ++p) {
+    if (p == me) {
+      w.peer_host[p] = w.base;
+      continue;
+    }
+    void* ptr = nullptr;
+    MOE_CUDA(cudaIpcOpenMemHandle(&ptr, all[p], cudaIpcMemLazyEnablePeerAccess));
+    w.peer_host[p] = static_cast<uint8_t*>(ptr);
+  }
+  MOE_CUDA(cudaMalloc(&w.peer_dev, P * sizeof(uint8_t*)));
+  MOE_CUDA(cudaMemcpy(w.peer_dev, w.peer_host, P * sizeof(uint8_t*), cudaMemcpyHostToDevice));
+  // every rank has mapped every window before anyone writes into one
+  int32_t* one = nullptr;
+  MOE_CUDA(cudaMalloc(&one, 4));
+  P2P_NCCL(ncclAllReduce(one, one, 1, ncclInt32, ncclSum, (ncclComm_t)nccl_comm, st));
+  MOE_CUDA(cudaStreamSynchronize(st));
+  MOE_CUDA(cudaFree(one));
+}
+
+void p2p_teardown(P2PWindow& w) {
+  for (uint32_t p = 0; p < w.P; ++p)
+    if (p != w.me && w.peer_host[p]) cudaIpcCloseMemHandle(w.peer_host[p]);
+  if (w.peer_dev) cudaFree(w.peer_dev);
+  if (w.base) cudaFree(w.base);
+  if (w.err) cudaFree(w.err);
+  w = P2PWindow{};
+}
+
+void p2p_wait(const P2PWindow& w, int slot, uint64_t target, cudaStream_t st) {
+  if (w.P <= 1) return;
+  p2p_wait_kernel<<<1, 32, 0, st>>>(reinterpret_cast<const uint64_t*>(w.base + w.off_flags), w.P,
+                                     w.me, slot, target, w.err);
+  MOE_LAUNCH_CHECK("p2p_wait_kernel");
+  count_launch();
+}
+
+void p2p_signal(const P2PWindow& w, int slot, uint64_t value, cudaStream_t st) {
+  if (w.P <= 1) return;
+  p2p_signal_kernel<<<1, 32, 0, st>>>(win_of(w), slot, value);
+  MOE_LAUNCH_CHECK("p2p_signal_kernel");
+  count_launch();
+}
+
+void p2p_dispatch(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t E, uint32_t El, uint32_t k,
+                  uint64_t C, uint64_t Cs, moe_dtype_t dt, const void* x, const int32_t* expert,
+                  const int32_t* position, const int32_t* kept, int32_t* slot, uint64_t epoch,
+                  cudaStream_t st) {
+  const uint64_t ntb = ceil_div(T, 8);
+  const unsigned grid = (unsigned)(ntb + E);
+  if (dt == MOE_DTYPE_BF16)
+    p2p_dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        win_of(w), w.off_xr, w.off_cnt, ctr_of(w, 0), T, d, E, El, k, C, Cs,
+        (const __nv_bfloat16*)x, expert, position, kept, slot, ntb, epoch);
+  else
+    p2p_dispatch_kernel<float><<<grid, 256, 0, st>>>(win_of(w), w.off_xr, w.off_cnt, ctr_of(w, 0),
+                                                     T, d, E, El, k, C, Cs, (const float*)x, expert,
+                                                     position, kept, slot, ntb, epoch);
+  MOE_LAUNCH_CHECK("p2p_dispatch_kernel");
+  count_launch();
+}
+
+void p2p_combine_bwd(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t E, uint32_t El,
+                     uint32_t k, uint64_t C, uint64_t Cs, moe_dtype_t dt, const void* dy,
+                     const int32_t* slot, const float* gate, const int32_t* expert,
+                     const int32_t* position, const int32_t* kept, float* dgate, uint64_t epoch,
+                     cudaStream_t st) {
+  const uint64_t ntb = ceil_div(T, 8);
+  const unsigned grid = (unsigned)(ntb + E);
+  if (dt == MOE_DTYPE_BF16)
+    p2p_combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        win_of(w), w.off_dyr, w.off_yh, ctr_of(w, 1), T, d, E, El, k, C, Cs,
+        (const __nv_bfloat16*)dy, slot, gate, expert, position, kept, dgate, ntb, epoch);
+  else
+    p2p_combine_bwd_kernel<float><<<grid, 256, 0, st>>>(
+        win_of(w), w.off_dyr, w.off_yh, ctr_of(w, 1), T, d, E, El, k, C, Cs, (const float*)dy,
+        slot, gate, expert, position, kept, dgate, ntb, epoch);
+  MOE_LAUNCH_CHECK("p2p_combine_bwd_kernel");
+  count_launch();
+}
+
+void p2p_push_home(const P2PWindow& w, uint64_t home_off, const void* src, uint32_t El,
+                   uint64_t Cs, uint32_t d, uint64_t esz, int slot, uint64_t epoch,
+                   cudaStream_t st) {
+  dim3 grid(w.P * El, (unsigned)ceil_div(Cs, 32));
+  p2p_push_kernel<<<grid, 256, 0, st>>>(win_of(w), home_off, w.off_cnt,
+                                        ctr_of(w, slot == SLOT_Y ? 2 : 3),
+                                        static_cast<const uint8_t*>(src), (int)El, Cs, d * esz,
+                                        slot, epoch);
+  MOE_LAUNCH_CHECK("p2p_push_kernel");
+  count_launch();
+}
+
+}  // namespace moe

@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "ep_p2p.h"
 #include "layer.h"
 
 namespace moe {
@@ -109,9 +110,23 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   rws.rank_local = dalloc<int32_t>(owned, T * k);
   // token buffers
   const uint64_t slot_bytes = (uint64_t)E * Cs * dm * esz;
-  xs = dalloc_bytes(owned, slot_bytes);
-  xr = P > 1 ? dalloc_bytes(owned, slot_bytes) : xs;
-  cnt_recv = P > 1 ? dalloc<int32_t>(owned, E) : kept;
+  p2p = P > 1 && d.exchange == MOE_EXCHANGE_P2P;
+  config_check(d.exchange == MOE_EXCHANGE_P2P || d.exchange == MOE_EXCHANGE_NCCL,
+               "layer.exchange: must be MOE_EXCHANGE_P2P or MOE_EXCHANGE_NCCL");
+  if (p2p) {
+    // receive / home buffers live in one IPC window that every peer maps
+    p2p_setup(win, comm, P, rank, slot_bytes, slot_bytes, E, 0);
+    xr = win.base + win.off_xr;
+    dYr = win.base + win.off_dyr;
+    Yh = win.base + win.off_yh;
+    dXh = win.base + win.off_dxh;
+    cnt_recv = reinterpret_cast<int32_t*>(win.base + win.off_cnt);
+  }
+  if (!p2p) {
+    xs = dalloc_bytes(owned, slot_bytes);
+    xr = P > 1 ? dalloc_bytes(owned, slot_bytes) : xs;
+    cnt_recv = P > 1 ? dalloc<int32_t>(owned, E) : kept;
+  }
   gm = dalloc<int32_t>(owned, E);
   ga = dalloc<int32_t>(owned, E);
   gb = dalloc<int32_t>(owned, E);
@@ -121,25 +136,28 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   Gp = dalloc_bytes(owned, rows * dff * esz);
   Aact = dalloc_bytes(owned, rows * dff * esz);
   Yl = dalloc_bytes(owned, slot_bytes);
-  Yh = P > 1 ? dalloc_bytes(owned, slot_bytes) : Yl;
+  if (!p2p) Yh = P > 1 ? dalloc_bytes(owned, slot_bytes) : Yl;
   // backward
   dgate = dalloc<float>(owned, T * k);
-  dYs = dalloc_bytes(owned, slot_bytes);
-  dYr = P > 1 ? dalloc_bytes(owned, slot_bytes) : dYs;
+  if (!p2p) {
+    dYs = dalloc_bytes(owned, slot_bytes);
+    dYr = P > 1 ? dalloc_bytes(owned, slot_bytes) : dYs;
+  }
   dH = dalloc_bytes(owned, rows * dff * esz);
   dXl = dalloc_bytes(owned, slot_bytes);
-  dXh = P > 1 ? dalloc_bytes(owned, slot_bytes) : dXl;
+  if (!p2p) dXh = P > 1 ? dalloc_bytes(owned, slot_bytes) : dXl;
   if (dt == MOE_DTYPE_BF16) dl_lp = dalloc_bytes(owned, T * Epad * 2);
   else dl_f32 = dalloc<float>(owned, T * E);
   // Every row of the activation buffers holds finite values from here on, so
-  // zero pad rows of the partner operand annihilate them in the RAGGED_K GEMMs.
-  MOE_CUDA(cudaMemset(xs, 0, slot_bytes));
-  if (xr != xs) MOE_CUDA(cudaMemset(xr, 0, slot_bytes));
+  // zero pad rows of the partner operand annihilate them in the RAGGED_K GEMMs
+  // (the P2P window is zeroed by p2p_setup).
+  if (xs) MOE_CUDA(cudaMemset(xs, 0, slot_bytes));
+  if (!p2p && xr != xs) MOE_CUDA(cudaMemset(xr, 0, slot_bytes));
   MOE_CUDA(cudaMemset(Gp, 0, rows * dff * esz));
   MOE_CUDA(cudaMemset(Aact, 0, rows * dff * esz));
   MOE_CUDA(cudaMemset(dH, 0, rows * dff * esz));
-  MOE_CUDA(cudaMemset(dYs, 0, slot_bytes));
-  if (dYr != dYs) MOE_CUDA(cudaMemset(dYr, 0, slot_bytes));
+  if (dYs) MOE_CUDA(cudaMemset(dYs, 0, slot_bytes));
+  if (!p2p && dYr != dYs) MOE_CUDA(cudaMemset(dYr, 0, slot_bytes));
   // gate GEMM tables: one group of T rows; split-K groups for dwg
   {
     std::vector<int32_t> one = {(int32_t)T, 0, 0, 0};
@@ -164,6 +182,10 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
 }
 
 Layer::~Layer() {
+  if (p2p) {
+    cudaDeviceSynchronize();
+    p2p_teardown(win);
+  }
   for (int i = 0; i < kMaxPhases + 1; ++i) cudaEventDestroy(ev[i]);
   for (void* p : owned) cudaFree(p);
   if (x_stage) cudaFree(x_stage);
@@ -204,6 +226,8 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   nphase = 0;
   x_saved_ptr = x;
   if (profiling) MOE_CUDA(cudaEventRecord(ev[0], st));
+  const uint64_t ph = ++phase;
+  if (p2p) p2p_wait(win, SLOT_PHASE, ph - 1, st);  // peers done reading our previous writes
   // K1: logits = x wg^T (+ bg), fp32 out
   if (override_logits) {
     MOE_CUDA(cudaMemcpyAsync(logits, override_logits, T * E * 4, cudaMemcpyDeviceToDevice, st));
@@ -235,11 +259,18 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   moe_routing_out_t ro{expert, gate, position, keep, count1, count2, kept, aux};
   route_forward(T, E, k, C, logits, ro, rws, st);
   mark("route", st);
-  // K3: dispatch into the Fusion-packed send buffer
-  dispatch_tokens(T, dm, E, k, C, pad, dt, x, expert, position, kept, xs, slot, st);
-  mark("dispatch", st);
+  // K3 (+K4 in P2P mode): dispatch into the Fusion-packed send buffer, or
+  // straight into the owning ranks' receive buffers over NVLink
+  if (p2p) {
+    p2p_dispatch(win, T, dm, E, El, k, C, Cs, dt, x, expert, position, kept, slot, ph, st);
+    mark("dispatch_p2p", st);
+    p2p_wait(win, SLOT_DISPATCH, ph, st);
+  } else {
+    dispatch_tokens(T, dm, E, k, C, pad, dt, x, expert, position, kept, xs, slot, st);
+    mark("dispatch", st);
+  }
   // K4: counts + payload exchange (one message per peer)
-  if (P > 1) {
+  if (P > 1 && !p2p) {
     MOE_NCCL(ncclGroupStart());
     a2a(kept, cnt_recv, El * sizeof(int32_t), st);
     a2a(xs, xr, El * Cs * dm * esz, st);
@@ -275,11 +306,17 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     grouped_gemm(p, st);
   }
   mark("ffn2", st);
-  if (P > 1) a2a(Yl, Yh, El * Cs * dm * esz, st);
+  if (p2p) {
+    p2p_push_home(win, win.off_yh, Yl, El, Cs, dm, esz, SLOT_Y, ph, st);
+    p2p_wait(win, SLOT_Y, ph, st);
+  } else if (P > 1) {
+    a2a(Yl, Yh, El * Cs * dm * esz, st);
+  }
   mark("a2a_combine", st);
   // K6: weighted combine
   combine_tokens(T, dm, k, dt, Yh, slot, gate, y, st);
   mark("combine", st);
+  if (p2p) p2p_signal(win, SLOT_PHASE, ph, st);
   if (logits_out)
     MOE_CUDA(cudaMemcpyAsync(logits_out, logits, T * E * 4, cudaMemcpyDeviceToDevice, st));
   if (rout) {
@@ -306,8 +343,16 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   arg_check(w.wg != nullptr, "backward.params.wg: gate weight required");
   nphase = 0;
   if (profiling) MOE_CUDA(cudaEventRecord(ev[0], st));
-  // K6^T: dgate and the gate-scaled dY into the send layout (+ zero pad rows)
-  combine_backward(T, dm, E, k, C, pad, dt, dy, Yh, slot, gate, kept, dYs, dgate, st);
+  const uint64_t ph = ++phase;
+  // K6^T: dgate and the gate-scaled dY into the send layout (+ zero pad rows),
+  // or straight into the owning ranks' receive buffers (P2P)
+  if (p2p) {
+    p2p_wait(win, SLOT_PHASE, ph - 1, st);
+    p2p_combine_bwd(win, T, dm, E, El, k, C, Cs, dt, dy, slot, gate, expert, position, kept,
+                    dgate, ph, st);
+  } else {
+    combine_backward(T, dm, E, k, C, pad, dt, dy, Yh, slot, gate, kept, dYs, dgate, st);
+  }
   mark("combine_bwd", st);
   // K2^T: dlogits
   if (desc.has_gate_bias && g.dbg) MOE_CUDA(cudaMemsetAsync(g.dbg, 0, E * 4, st));
@@ -315,7 +360,8 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
                  dt == MOE_DTYPE_BF16 ? MOE_DTYPE_BF16 : MOE_DTYPE_F32,
                  dt == MOE_DTYPE_BF16 ? Epad : E, desc.has_gate_bias ? g.dbg : nullptr, st);
   mark("route_bwd", st);
-  if (P > 1) a2a(dYs, dYr, El * Cs * dm * esz, st);
+  if (p2p) p2p_wait(win, SLOT_DY, ph, st);
+  else if (P > 1) a2a(dYs, dYr, El * Cs * dm * esz, st);
   mark("a2a_dy", st);
   // K5^T dgrad: dH = (dY W2) * gelu'(h) (stored by ffn1), db1 = column sums
   // of dH fused into the same epilogue; dXe = dH W1
@@ -348,7 +394,8 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("dgrad_ffn1", st);
-  if (P > 1) a2a(dXl, dXh, El * Cs * dm * esz, st);
+  if (p2p) p2p_push_home(win, win.off_dxh, dXl, El, Cs, dm, esz, SLOT_DX, ph, st);
+  else if (P > 1) a2a(dXl, dXh, El * Cs * dm * esz, st);
   mark("a2a_dx", st);
   // K5^T wgrad: dW1[j] = sum dH^T X, dW2[j] = sum dY^T A (RAGGED_K over slices)
   {
@@ -383,6 +430,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   }
   group_colsum(P * El, gm, ga, gb, El, dm, dt, dYr, g.db2, st, Cs);
   mark("bias_grads", st);
+  if (p2p) p2p_wait(win, SLOT_DX, ph, st);
   // gate dgrad with the combine backward folded into its epilogue:
   // dx[t] = dlogits[t] wg + sum_i dXe[slot_i]; dwg = dlogits^T x (split-K)
   if (T) {
@@ -447,6 +495,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     MOE_NCCL(ncclGroupEnd());
   }
   mark("allreduce_gate", st);
+  if (p2p) p2p_signal(win, SLOT_PHASE, ph, st);
 }
 
 void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, const void* dy_host,

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <vector>
 
+#include "ep_p2p.h"
 #include "kernels.h"
 #include "moe_b200.h"
 
@@ -40,6 +41,9 @@ struct Layer {
   uint64_t esz = 2;
   void* comm = nullptr;
   int device = 0;
+  bool p2p = false;       // EP exchange over NVLink peer memory
+  P2PWindow win;
+  uint64_t phase = 0;     // forward/backward phase counter (P2P epochs)
 
   std::vector<void*> owned;
   // routing state

@@ -69,6 +69,7 @@ class MoEConfig:
     tokens: int
     dtype: torch.dtype = torch.bfloat16
     gate_bias: bool = False
+    exchange: str = "p2p"  # EP token exchange: "p2p" (NVLink peer stores) or "nccl"
 
 
 class EPGroup:
@@ -125,6 +126,9 @@ class MoELayer:
         desc.ep_size = self.P
         desc.ep_rank = self.rank
         desc.nccl_comm = ep.comm if ep else None
+        if cfg.exchange not in ("p2p", "nccl"):
+            raise _lib.ConfigError("layer.exchange: must be 'p2p' or 'nccl'")
+        desc.exchange = 0 if cfg.exchange == "p2p" else 1
         h = C.c_void_p()
         if self.device.type == "cuda":
             with torch.cuda.device(self.device):

@@ -51,14 +51,15 @@ def _worker(rank, world, port, case, q):
                     assert torch.equal(recv[s * nn:(s + 1) * nn], allsend[s][rank * n:rank * n + nn])
             q.put((rank, "ok"))
             return
-        E, k, d, dff, T, dt = case
-        cfg = MoEConfig(E, k, d, dff, 1.25, T, dt)
+        E, k, d, dff, T, dt, exch = case
+        cfg = MoEConfig(E, k, d, dff, 1.25, T, dt, exchange=exch)
         lep = MoELayer(cfg, ep=ep)
         lep.init_params(99)
         x = lep.make_input(99)
         dy = lep.make_input(99, T_DY)
-        y = lep.forward(x)
-        dx = lep.backward(dy, d_aux=0.02)
+        for _ in range(3):  # repeated steps exercise the P2P epoch/phase protocol
+            y = lep.forward(x)
+            dx = lep.backward(dy, d_aux=0.02)
         # single-GPU layer with all experts, same tokens
         l1 = MoELayer(cfg)
         l1.init_params(99)
@@ -112,9 +113,12 @@ def test_packed_alltoall_fused_and_unfused():
 
 
 @pytest.mark.parametrize("case", [
-    (8, 2, 256, 512, 1024, torch.bfloat16),
-    (64, 1, 1024, 4096, 8192, torch.bfloat16),
-    (8, 2, 128, 256, 512, torch.float32),
+    (8, 2, 256, 512, 1024, torch.bfloat16, "p2p"),
+    (8, 2, 256, 512, 1024, torch.bfloat16, "nccl"),
+    (64, 1, 1024, 4096, 8192, torch.bfloat16, "p2p"),
+    (64, 1, 1024, 4096, 8192, torch.bfloat16, "nccl"),
+    (8, 2, 128, 256, 512, torch.float32, "p2p"),
+    (32, 2, 256, 512, 3000, torch.bfloat16, "p2p"),
 ])
 def test_ep_layer_matches_single_gpu(case):
     _run(case, world=min(torch.cuda.device_count(), 2))
