@@ -281,7 +281,12 @@ moe_status_t moe_layer_backward(moe_layer_t layer, const moe_layer_params_t* par
 
 /* One training step of the layer from HOST buffers (the end-to-end API):
  * H2D x_host, dy_host (pinned) -> forward + backward -> D2H y_host, dx_host.
- * Parameter gradients stay on the device in `grads`.  Enqueued on `stream`. */
+ * Parameter gradients stay on the device in `grads`.  Runs on the layer's own
+ * copy-in / compute / copy-out streams over double-buffered staging so that
+ * consecutive calls overlap H2D, compute and D2H; `stream` is made to wait for
+ * this step's D2H, i.e. outputs, gradients and the reuse of the host buffers
+ * are safe once `stream` reaches this call.  Do not interleave with
+ * moe_layer_forward/backward on the same layer without synchronising. */
 moe_status_t moe_layer_train_step_host(moe_layer_t layer, const moe_layer_params_t* params,
                                        const void* x_host, const void* dy_host, float d_aux,
                                        void* y_host, void* dx_host, const moe_layer_grads_t* grads,

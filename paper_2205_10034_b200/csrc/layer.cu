@@ -188,7 +188,13 @@ Layer::~Layer() {
   }
   for (int i = 0; i < kMaxPhases + 1; ++i) cudaEventDestroy(ev[i]);
   for (void* p : owned) cudaFree(p);
-  if (x_stage) cudaFree(x_stage);
+  if (x_stage) {
+    for (int i = 0; i < 3; ++i) cudaStreamSynchronize(hp_stream[i]);
+    cudaFree(x_stage);
+    for (int i = 0; i < 3; ++i) cudaStreamDestroy(hp_stream[i]);
+    for (int bb = 0; bb < 2; ++bb)
+      for (int i = 0; i < 3; ++i) cudaEventDestroy(hp_ev[bb][i]);
+  }
 }
 
 void Layer::mark(const char* name, cudaStream_t st) {
@@ -501,22 +507,43 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
 void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, const void* dy_host,
                             float d_aux, void* y_host, void* dx_host, const moe_layer_grads_t& g,
                             cudaStream_t st) {
+  // Three-stream pipeline over double-buffered staging: H2D of step i+1 and
+  // D2H of step i-1 overlap the compute of step i (PCIe is full duplex and the
+  // copy engines need no SMs).  The caller's stream waits for this step's D2H,
+  // so y_host / dx_host / the gradients are valid once `st` reaches this call.
   const uint64_t bytes = T * dm * esz;
   if (!x_stage) {
-    MOE_CUDA(cudaMalloc(&x_stage, 4 * bytes + 64));
+    MOE_CUDA(cudaMalloc(&x_stage, 8 * bytes + 64));
+    for (int i = 0; i < 3; ++i) MOE_CUDA(cudaStreamCreateWithFlags(&hp_stream[i], cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b)
+      for (int i = 0; i < 3; ++i)
+        MOE_CUDA(cudaEventCreateWithFlags(&hp_ev[b][i], cudaEventDisableTiming));
+    // the first step's copies must not start before work already queued on st
+    MOE_CUDA(cudaEventRecord(hp_ev[0][2], st));
+    MOE_CUDA(cudaStreamWaitEvent(hp_stream[0], hp_ev[0][2], 0));
+    MOE_CUDA(cudaStreamWaitEvent(hp_stream[1], hp_ev[0][2], 0));
   }
-  uint8_t* base = static_cast<uint8_t*>(x_stage);
+  cudaStream_t h2d = hp_stream[0], comp = hp_stream[1], d2h = hp_stream[2];
+  const int b = (int)(hp_iter & 1);
+  uint8_t* base = static_cast<uint8_t*>(x_stage) + (uint64_t)b * 4 * bytes;
   void* xd = base;
   void* dyd = base + bytes;
   void* yd = base + 2 * bytes;
   void* dxd = base + 3 * bytes;
-  MOE_CUDA(cudaMemcpyAsync(xd, x_host, bytes, cudaMemcpyHostToDevice, st));
-  MOE_CUDA(cudaMemcpyAsync(dyd, dy_host, bytes, cudaMemcpyHostToDevice, st));
-  x_saved_ptr = xd;
-  forward(w, xd, yd, nullptr, nullptr, nullptr, st);
-  backward(w, dyd, d_aux, dxd, g, st);
-  MOE_CUDA(cudaMemcpyAsync(y_host, yd, bytes, cudaMemcpyDeviceToHost, st));
-  MOE_CUDA(cudaMemcpyAsync(dx_host, dxd, bytes, cudaMemcpyDeviceToHost, st));
+  if (hp_iter >= 2) MOE_CUDA(cudaStreamWaitEvent(h2d, hp_ev[b][2], 0));  // stage b drained
+  MOE_CUDA(cudaMemcpyAsync(xd, x_host, bytes, cudaMemcpyHostToDevice, h2d));
+  MOE_CUDA(cudaMemcpyAsync(dyd, dy_host, bytes, cudaMemcpyHostToDevice, h2d));
+  MOE_CUDA(cudaEventRecord(hp_ev[b][0], h2d));
+  MOE_CUDA(cudaStreamWaitEvent(comp, hp_ev[b][0], 0));
+  forward(w, xd, yd, nullptr, nullptr, nullptr, comp);
+  backward(w, dyd, d_aux, dxd, g, comp);
+  MOE_CUDA(cudaEventRecord(hp_ev[b][1], comp));
+  MOE_CUDA(cudaStreamWaitEvent(d2h, hp_ev[b][1], 0));
+  MOE_CUDA(cudaMemcpyAsync(y_host, yd, bytes, cudaMemcpyDeviceToHost, d2h));
+  MOE_CUDA(cudaMemcpyAsync(dx_host, dxd, bytes, cudaMemcpyDeviceToHost, d2h));
+  MOE_CUDA(cudaEventRecord(hp_ev[b][2], d2h));
+  MOE_CUDA(cudaStreamWaitEvent(st, hp_ev[b][2], 0));
+  ++hp_iter;
 }
 
 // --------------------------------------------------------------- comm -----

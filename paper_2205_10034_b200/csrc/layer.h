@@ -70,7 +70,10 @@ struct Layer {
   int32_t *split_m = nullptr, *split_a = nullptr, *split_b = nullptr;
   uint32_t nsplit = 1;
   const void* x_saved_ptr = nullptr;
-  void* x_stage = nullptr;
+  void* x_stage = nullptr;          // host-buffer pipeline: 2 x (x, dy, y, dx)
+  cudaStream_t hp_stream[3] = {};   // h2d, compute, d2h
+  cudaEvent_t hp_ev[2][3] = {};     // per stage: h2d done, compute done, d2h done
+  uint64_t hp_iter = 0;
   bool has_forward = false;
   // profiling
   bool profiling = false;

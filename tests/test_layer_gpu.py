@@ -174,3 +174,29 @@ def test_layer_full_size_vs_torch_fp32(E, k, d, dff, T):
             "dw1": err(g["dw1"], rdw1), "db1": err(g["db1"], rdb1), "dw2": err(g["dw2"], rdw2),
             "db2": err(g["db2"], rdb2)}
     assert all(v <= 2e-2 for v in errs.values()), errs
+
+
+def test_train_step_host_pipeline_matches_device_calls():
+    """moe_layer_train_step_host (3-stream, double-buffered) == forward/backward."""
+    cfg = MoEConfig(16, 2, 256, 512, 1.25, 2048, torch.bfloat16)
+    layer = MoELayer(cfg)
+    layer.init_params(5)
+    xs = [layer.make_input(100 + i) for i in range(3)]
+    dys = [layer.make_input(200 + i, T_DY) for i in range(3)]
+    ref = []
+    for x, dy in zip(xs, dys):
+        y = layer.forward(x)
+        dx = layer.backward(dy, d_aux=0.01)
+        ref.append((y.cpu(), dx.cpu(), layer.grads["dw1"].cpu().clone()))
+    torch.cuda.synchronize()
+    hx = [x.cpu().pin_memory() for x in xs]
+    hdy = [d.cpu().pin_memory() for d in dys]
+    hy = [torch.empty_like(h).pin_memory() for h in hx]
+    hdx = [torch.empty_like(h).pin_memory() for h in hx]
+    for i in range(3):
+        layer.train_step_host(hx[i], hdy[i], hy[i], hdx[i], d_aux=0.01)
+    torch.cuda.current_stream().synchronize()
+    for i in range(3):
+        assert torch.equal(hy[i], ref[i][0]) and torch.equal(hdx[i], ref[i][1]), i
+    err = (layer.grads["dw1"].cpu() - ref[2][2]).abs().max() / ref[2][2].abs().max()
+    assert err < 1e-5
