@@ -4,6 +4,12 @@
 // the exchange is fused into the kernels that produce the rows, moves exactly
 // the kept rows (no capacity padding on the wire) and needs no host sync.
 //
+// Per phase the kept counts are all-gathered first (E int32 per rank, one
+// tiny peer-store kernel) so every sender knows where its rows start inside
+// the receiver's per-expert region: rows of source s for expert e land at
+// offset sum_{s' < s} cnt[s'][e].  Each local expert is then ONE contiguous
+// GEMM group for any number of ranks (no per-(source, expert) tile quantisation).
+//
 // Ordering: every producing kernel ends with a grid-wide "last block" step that
 // publishes `epoch` into each destination's flags[slot][me] with a
 // system-scope release store after all its remote stores are fenced
@@ -13,8 +19,8 @@
 // (SLOT_PHASE), which is when it last read the buffers this phase overwrites.
 // Spins time out after 30 s with __trap() rather than hanging the device.
 //
-// Layout and receive order follow alltoall_flat (collectives.cpp:10-21): rank
-// r's receive buffer is [src][local expert][Cs][d], i.e. sources in rank order.
+// Receive order follows alltoall_flat (collectives.cpp:10-21): sources in rank
+// order inside every expert region.
 #include <cstring>
 #include <string>
 #include <vector>
@@ -43,15 +49,19 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
+// Kernel-side view of the window (by value).
 struct Win {
   uint8_t** peers;
-  uint64_t off_flags;
-  uint32_t P, me;
+  uint64_t off_xr, off_dyr, off_cnt, off_flags;
+  uint32_t P, me, E, El;
+  uint64_t Cs, Rmax, row_bytes;
 };
 
-__device__ __forceinline__ uint64_t* flag_at(uint8_t* base, uint64_t off_flags, uint32_t P,
-                                             int slot, uint32_t src) {
-  return reinterpret_cast<uint64_t*>(base + off_flags) + (uint64_t)slot * P + src;
+__device__ __forceinline__ uint64_t* flag_at(uint8_t* base, const Win& w, int slot, uint32_t src) {
+  return reinterpret_cast<uint64_t*>(base + w.off_flags) + (uint64_t)slot * w.P + src;
+}
+__device__ __forceinline__ const int32_t* cnt_of(const Win& w) {
+  return reinterpret_cast<const int32_t*>(w.peers[w.me] + w.off_cnt);
 }
 
 // All threads of every block call this exactly once at the end of a producing
@@ -65,7 +75,7 @@ __device__ void grid_done_signal(const Win& w, uint32_t* ctr, int slot, uint64_t
     if (prev == nb - 1) {
       __threadfence_system();
       for (uint32_t p = 0; p < w.P; ++p)
-        if (p != w.me) st_release_sys(flag_at(w.peers[p], w.off_flags, w.P, slot, w.me), value);
+        if (p != w.me) st_release_sys(flag_at(w.peers[p], w, slot, w.me), value);
       atomicExch(ctr, 0u);
     }
   }
@@ -91,67 +101,87 @@ __global__ void p2p_wait_kernel(const uint64_t* flags, uint32_t P, uint32_t me, 
 __global__ void p2p_signal_kernel(Win w, int slot, uint64_t value) {
   __threadfence_system();
   const uint32_t p = threadIdx.x;
-  if (p < w.P && p != w.me) st_release_sys(flag_at(w.peers[p], w.off_flags, w.P, slot, w.me), value);
+  if (p < w.P && p != w.me) st_release_sys(flag_at(w.peers[p], w, slot, w.me), value);
 }
 
-template <typename T>
-struct V8;  // elements per 16B vector
-template <>
-struct V8<__nv_bfloat16> {
-  static constexpr int N = 8;
-};
-template <>
-struct V8<float> {
-  static constexpr int N = 4;
-};
+// kept[E] -> cnt[me][:] on every rank (including this one)
+__global__ void p2p_counts_kernel(Win w, uint32_t* ctr, const int32_t* __restrict__ kept,
+                                  uint64_t epoch) {
+  for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) {
+    const int32_t n = kept[e];
+    for (uint32_t p = 0; p < w.P; ++p)
+      reinterpret_cast<int32_t*>(w.peers[p] + w.off_cnt)[(uint64_t)w.me * w.E + e] = n;
+  }
+  grid_done_signal(w, ctr, SLOT_CNT, epoch);
+}
 
-// grid: [0, ntb) token blocks (8 warps, warp per token) + E expert blocks
+// offset of source `me`'s rows inside expert e's region on its owner
+__device__ __forceinline__ int src_offset(const int32_t* cnt, uint32_t E, uint32_t me, int e) {
+  int off = 0;
+  for (uint32_t s = 0; s < me; ++s) off += cnt[(uint64_t)s * E + e];
+  return off;
+}
+
+constexpr int MAXE = 256;
+
+// grid: ceil(T/8) blocks, warp per token
 template <typename T>
 __global__ void __launch_bounds__(256) p2p_dispatch_kernel(
-    Win w, uint64_t off_xr, uint64_t off_cnt, uint32_t* ctr, uint64_t T_, int d, int E, int El,
-    int k, uint64_t C, uint64_t Cs, const T* __restrict__ x, const int32_t* __restrict__ expert,
-    const int32_t* __restrict__ position, const int32_t* __restrict__ kept,
-    int32_t* __restrict__ slot, uint64_t ntb, uint64_t epoch) {
+    Win w, uint32_t* ctr, uint64_t T_, int d, int k, uint64_t C, const T* __restrict__ x,
+    const int32_t* __restrict__ expert, const int32_t* __restrict__ position,
+    int32_t* __restrict__ slot, uint64_t epoch) {
+  __shared__ int off_s[MAXE];
+  const int32_t* cnt = cnt_of(w);
+  for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) off_s[e] = src_offset(cnt, w.E, w.me, e);
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = d / V8<T>::N;
-  if (blockIdx.x < ntb) {
-    const uint64_t t = blockIdx.x * 8ull + warp;
-    if (t < T_) {
-      uint4* dst[2] = {nullptr, nullptr};
+  const int nv = (int)(w.row_bytes / 16);
+  const uint64_t t = blockIdx.x * 8ull + warp;
+  if (t < T_) {
+    uint4* dst[2] = {nullptr, nullptr};
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        if (i >= k) break;
-        const int e = expert[t * k + i];
-        const int p = position[t * k + i];
-        const bool keep = (uint64_t)p < C;
-        if (lane == 0) slot[t * k + i] = keep ? (int32_t)(e * Cs + p) : -1;
-        if (keep) {
-          const int r = e / El, j = e % El;
-          const uint64_t row = ((uint64_t)w.me * El + j) * Cs + p;
-          dst[i] = reinterpret_cast<uint4*>(w.peers[r] + off_xr + row * d * sizeof(T));
-        }
-      }
-      const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
-      for (int v = lane; v < nv; v += 32) {
-        const uint4 val = __ldg(src + v);
-        if (dst[0]) dst[0][v] = val;
-        if (dst[1]) dst[1][v] = val;
+    for (int i = 0; i < 2; ++i) {
+      if (i >= k) break;
+      const int e = expert[t * k + i];
+      const int p = position[t * k + i];
+      const bool keep = (uint64_t)p < C;
+      if (lane == 0) slot[t * k + i] = keep ? (int32_t)(e * w.Cs + p) : -1;
+      if (keep) {
+        const int r = e / (int)w.El, j = e % (int)w.El;
+        const uint64_t row = (uint64_t)j * w.Rmax + off_s[e] + p;
+        dst[i] = reinterpret_cast<uint4*>(w.peers[r] + w.off_xr + row * w.row_bytes);
       }
     }
-  } else {
-    const int e = (int)(blockIdx.x - ntb);
-    const int r = e / El, j = e % El;
-    const int n = kept[e];
-    const uint64_t base_row = ((uint64_t)w.me * El + j) * Cs;
-    if (threadIdx.x == 0)
-      reinterpret_cast<int32_t*>(w.peers[r] + off_cnt)[w.me * El + j] = n;
-    const int end = (int)min((uint64_t)((n + 63) / 64) * 64, Cs);
-    for (int rr = n + warp; rr < end; rr += 8) {
-      uint4* row = reinterpret_cast<uint4*>(w.peers[r] + off_xr + (base_row + rr) * d * sizeof(T));
-      for (int v = lane; v < nv; v += 32) row[v] = make_uint4(0, 0, 0, 0);
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
+    for (int v = lane; v < nv; v += 32) {
+      const uint4 val = __ldg(src + v);
+      if (dst[0]) dst[0][v] = val;
+      if (dst[1]) dst[1][v] = val;
     }
   }
   grid_done_signal(w, ctr, SLOT_DISPATCH, epoch);
+}
+
+// one block per local expert: group tables + zero pad rows [m, round64(m))
+__global__ void p2p_local_groups_kernel(Win w, int32_t* gm, int32_t* ga, int32_t* gb,
+                                        uint8_t* buf) {
+  const int j = blockIdx.x;
+  const int e = (int)(w.me * w.El) + j;
+  const int32_t* cnt = cnt_of(w);
+  int m = 0;
+  for (uint32_t s = 0; s < w.P; ++s) m += cnt[(uint64_t)s * w.E + e];
+  if (threadIdx.x == 0) {
+    gm[j] = m;
+    ga[j] = (int32_t)(j * w.Rmax);
+    gb[j] = j;
+  }
+  const int end = (int)min((uint64_t)((m + 63) / 64) * 64, w.Rmax);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nv = (int)(w.row_bytes / 16);
+  for (int r = m + warp; r < end; r += nw) {
+    uint4* row = reinterpret_cast<uint4*>(buf + ((uint64_t)j * w.Rmax + r) * w.row_bytes);
+    for (int v = lane; v < nv; v += 32) row[v] = make_uint4(0, 0, 0, 0);
+  }
 }
 
 template <typename T>
@@ -189,74 +219,67 @@ __device__ __forceinline__ void st8<float>(float* p, const float (&f)[8]) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) p2p_combine_bwd_kernel(
-    Win w, uint64_t off_dyr, uint64_t off_yh, uint32_t* ctr, uint64_t T_, int d, int E, int El,
-    int k, uint64_t C, uint64_t Cs, const T* __restrict__ dy, const int32_t* __restrict__ slot,
-    const float* __restrict__ gate, const int32_t* __restrict__ expert,
-    const int32_t* __restrict__ position, const int32_t* __restrict__ kept,
-    float* __restrict__ dgate, uint64_t ntb, uint64_t epoch) {
+    Win w, uint64_t off_yh, uint32_t* ctr, uint64_t T_, int d, int k, const T* __restrict__ dy,
+    const int32_t* __restrict__ slot, const float* __restrict__ gate,
+    const int32_t* __restrict__ expert, const int32_t* __restrict__ position,
+    float* __restrict__ dgate, uint64_t epoch) {
+  __shared__ int off_s[MAXE];
+  const int32_t* cnt = cnt_of(w);
+  for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) off_s[e] = src_offset(cnt, w.E, w.me, e);
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const T* Yh = reinterpret_cast<const T*>(w.peers[w.me] + off_yh);
-  if (blockIdx.x < ntb) {
-    const uint64_t t = blockIdx.x * 8ull + warp;
-    if (t < T_) {
-      for (int i = 0; i < k; ++i) {
-        const int32_t s = slot[t * k + i];
-        if (s < 0) {
-          if (lane == 0) dgate[t * k + i] = 0.f;
-          continue;
-        }
-        const int e = expert[t * k + i], p = position[t * k + i];
-        const int r = e / El, j = e % El;
-        T* dst = reinterpret_cast<T*>(w.peers[r] + off_dyr) +
-                 (((uint64_t)w.me * El + j) * Cs + p) * d;
-        const float g = gate[t * k + i];
-        float dot = 0.f;
-        for (int c = lane * 8; c < d; c += 256) {
-          float a[8], b[8], o[8];
-          ld8<T>(dy + t * d + c, a);
-          ld8<T>(Yh + (uint64_t)s * d + c, b);
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            dot = fmaf(a[q], b[q], dot);
-            o[q] = g * a[q];
-          }
-          st8<T>(dst + c, o);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        if (lane == 0) dgate[t * k + i] = dot;
+  const uint64_t t = blockIdx.x * 8ull + warp;
+  if (t < T_) {
+    for (int i = 0; i < k; ++i) {
+      const int32_t s = slot[t * k + i];
+      if (s < 0) {
+        if (lane == 0) dgate[t * k + i] = 0.f;
+        continue;
       }
-    }
-  } else {
-    const int e = (int)(blockIdx.x - ntb);
-    const int r = e / El, j = e % El;
-    const int n = kept[e];
-    const uint64_t base_row = ((uint64_t)w.me * El + j) * Cs;
-    const int end = (int)min((uint64_t)((n + 63) / 64) * 64, Cs);
-    const int nv = d / V8<T>::N;
-    for (int rr = n + warp; rr < end; rr += 8) {
-      uint4* row = reinterpret_cast<uint4*>(w.peers[r] + off_dyr + (base_row + rr) * d * sizeof(T));
-      for (int v = lane; v < nv; v += 32) row[v] = make_uint4(0, 0, 0, 0);
+      const int e = expert[t * k + i], p = position[t * k + i];
+      const int r = e / (int)w.El, j = e % (int)w.El;
+      T* dst = reinterpret_cast<T*>(w.peers[r] + w.off_dyr) +
+               ((uint64_t)j * w.Rmax + off_s[e] + p) * d;
+      const float g = gate[t * k + i];
+      float dot = 0.f;
+      for (int c = lane * 8; c < d; c += 256) {
+        float a[8], b[8], o[8];
+        ld8<T>(dy + t * d + c, a);
+        ld8<T>(Yh + (uint64_t)s * d + c, b);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          dot = fmaf(a[q], b[q], dot);
+          o[q] = g * a[q];
+        }
+        st8<T>(dst + c, o);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (lane == 0) dgate[t * k + i] = dot;
     }
   }
   grid_done_signal(w, ctr, SLOT_DY, epoch);
 }
 
-// grid (P*El groups, row chunks of 32); warp per row
-__global__ void __launch_bounds__(256) p2p_push_kernel(Win w, uint64_t home_off, uint64_t off_cnt,
-                                                       uint32_t* ctr, const uint8_t* __restrict__ src,
-                                                       int El, uint64_t Cs, uint64_t row_bytes,
+// grid (El * P, row chunks of 64): (j, s) = (blockIdx.x / P, blockIdx.x % P)
+__global__ void __launch_bounds__(256) p2p_push_kernel(Win w, uint64_t home_off, uint32_t* ctr,
+                                                       const uint8_t* __restrict__ src,
                                                        int slot_id, uint64_t epoch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = blockIdx.x;
-  const int s = g / El, j = g % El;
-  const int cnt = reinterpret_cast<const int32_t*>(w.peers[w.me] + off_cnt)[g];
-  const int r0 = blockIdx.y * 32;
-  const uint64_t nv = row_bytes / 16;
-  for (int r = r0 + warp; r < min(cnt, r0 + 32); r += 8) {
-    const uint4* from = reinterpret_cast<const uint4*>(src + ((uint64_t)g * Cs + r) * row_bytes);
+  const int j = blockIdx.x / w.P, s = blockIdx.x % w.P;
+  const int e = (int)(w.me * w.El) + j;
+  const int32_t* cnt = cnt_of(w);
+  int off = 0;
+  for (int q = 0; q < s; ++q) off += cnt[(uint64_t)q * w.E + e];
+  const int n = cnt[(uint64_t)s * w.E + e];
+  const int r0 = blockIdx.y * 64;
+  const uint64_t nv = w.row_bytes / 16;
+  for (int r = r0 + warp; r < min(n, r0 + 64); r += 8) {
+    const uint4* from =
+        reinterpret_cast<const uint4*>(src + ((uint64_t)j * w.Rmax + off + r) * w.row_bytes);
     uint4* to = reinterpret_cast<uint4*>(w.peers[s] + home_off +
-                                         (((uint64_t)w.me * El + j) * Cs + r) * row_bytes);
+                                         ((uint64_t)e * w.Cs + r) * w.row_bytes);
     for (uint64_t v = lane; v < nv; v += 32) to[v] = __ldg(from + v);
   }
   grid_done_signal(w, ctr, slot_id, epoch);
@@ -264,7 +287,10 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(Win w, uint64_t home_off,
 
 uint64_t a256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 
-Win win_of(const P2PWindow& w) { return Win{w.peer_dev, w.off_flags, w.P, w.me}; }
+Win win_of(const P2PWindow& w) {
+  return Win{w.peer_dev, w.off_xr, w.off_dyr, w.off_cnt, w.off_flags, w.P, w.me, w.E, w.El,
+             w.Cs, w.Rmax, w.row_bytes};
+}
 uint32_t* ctr_of(const P2PWindow& w, int i) {
   return reinterpret_cast<uint32_t*>(w.base + w.off_ctr) + i;
 }
@@ -278,17 +304,26 @@ uint32_t* ctr_of(const P2PWindow& w, int i) {
       ::moe::fail(MOE_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));  \
   } while (0)
 
-void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint64_t slice_bytes,
-               uint64_t home_bytes, uint32_t E, cudaStream_t st) {
+void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t E, uint64_t Cs,
+               uint64_t row_bytes, cudaStream_t st) {
   config_check(P <= 8, "layer.ep_size: P2P exchange supports up to 8 GPUs of one box");
+  config_check(E <= (uint32_t)MAXE, "layer.num_experts: P2P exchange supports up to 256");
+  config_check(row_bytes % 16 == 0, "layer.d_model: rows must be a multiple of 16 bytes");
   w.P = P;
   w.me = me;
+  w.E = E;
+  w.El = E / P;
+  w.Cs = Cs;
+  w.Rmax = (uint64_t)P * Cs;
+  w.row_bytes = row_bytes;
+  const uint64_t region = (uint64_t)w.El * w.Rmax * row_bytes;  // == E * Cs rows
+  const uint64_t home = (uint64_t)E * Cs * row_bytes;
   w.off_xr = 0;
-  w.off_dyr = a256(w.off_xr + slice_bytes);
-  w.off_yh = a256(w.off_dyr + slice_bytes);
-  w.off_dxh = a256(w.off_yh + home_bytes);
-  w.off_cnt = a256(w.off_dxh + home_bytes);
-  w.off_flags = a256(w.off_cnt + (uint64_t)E * 4);
+  w.off_dyr = a256(w.off_xr + region);
+  w.off_yh = a256(w.off_dyr + region);
+  w.off_dxh = a256(w.off_yh + home);
+  w.off_cnt = a256(w.off_dxh + home);
+  w.off_flags = a256(w.off_cnt + (uint64_t)P * E * 4);
   w.off_ctr = a256(w.off_flags + (uint64_t)NSLOT * P * 8);
   w.bytes = w.off_ctr + 256;
   MOE_CUDA(cudaMalloc(&w.base, w.bytes));
@@ -348,51 +383,55 @@ void p2p_signal(const P2PWindow& w, int slot, uint64_t value, cudaStream_t st) {
   count_launch();
 }
 
-void p2p_dispatch(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t E, uint32_t El, uint32_t k,
-                  uint64_t C, uint64_t Cs, moe_dtype_t dt, const void* x, const int32_t* expert,
-                  const int32_t* position, const int32_t* kept, int32_t* slot, uint64_t epoch,
-                  cudaStream_t st) {
-  const uint64_t ntb = ceil_div(T, 8);
-  const unsigned grid = (unsigned)(ntb + E);
+void p2p_counts(const P2PWindow& w, const int32_t* kept, uint64_t epoch, cudaStream_t st) {
+  p2p_counts_kernel<<<1, 256, 0, st>>>(win_of(w), ctr_of(w, 4), kept, epoch);
+  MOE_LAUNCH_CHECK("p2p_counts_kernel");
+  count_launch();
+}
+
+void p2p_dispatch(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t k, uint64_t C,
+                  moe_dtype_t dt, const void* x, const int32_t* expert, const int32_t* position,
+                  int32_t* slot, uint64_t epoch, cudaStream_t st) {
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, ceil_div(T, 8));
   if (dt == MOE_DTYPE_BF16)
     p2p_dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-        win_of(w), w.off_xr, w.off_cnt, ctr_of(w, 0), T, d, E, El, k, C, Cs,
-        (const __nv_bfloat16*)x, expert, position, kept, slot, ntb, epoch);
+        win_of(w), ctr_of(w, 0), T, d, k, C, (const __nv_bfloat16*)x, expert, position, slot, epoch);
   else
-    p2p_dispatch_kernel<float><<<grid, 256, 0, st>>>(win_of(w), w.off_xr, w.off_cnt, ctr_of(w, 0),
-                                                     T, d, E, El, k, C, Cs, (const float*)x, expert,
-                                                     position, kept, slot, ntb, epoch);
+    p2p_dispatch_kernel<float><<<grid, 256, 0, st>>>(win_of(w), ctr_of(w, 0), T, d, k, C,
+                                                     (const float*)x, expert, position, slot, epoch);
   MOE_LAUNCH_CHECK("p2p_dispatch_kernel");
   count_launch();
 }
 
-void p2p_combine_bwd(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t E, uint32_t El,
-                     uint32_t k, uint64_t C, uint64_t Cs, moe_dtype_t dt, const void* dy,
-                     const int32_t* slot, const float* gate, const int32_t* expert,
-                     const int32_t* position, const int32_t* kept, float* dgate, uint64_t epoch,
+void p2p_local_groups(const P2PWindow& w, int32_t* gm, int32_t* ga, int32_t* gb, void* buf,
+                      cudaStream_t st) {
+  p2p_local_groups_kernel<<<w.El, 256, 0, st>>>(win_of(w), gm, ga, gb, static_cast<uint8_t*>(buf));
+  MOE_LAUNCH_CHECK("p2p_local_groups_kernel");
+  count_launch();
+}
+
+void p2p_combine_bwd(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t k, moe_dtype_t dt,
+                     const void* dy, const int32_t* slot, const float* gate,
+                     const int32_t* expert, const int32_t* position, float* dgate, uint64_t epoch,
                      cudaStream_t st) {
-  const uint64_t ntb = ceil_div(T, 8);
-  const unsigned grid = (unsigned)(ntb + E);
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, ceil_div(T, 8));
   if (dt == MOE_DTYPE_BF16)
     p2p_combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-        win_of(w), w.off_dyr, w.off_yh, ctr_of(w, 1), T, d, E, El, k, C, Cs,
-        (const __nv_bfloat16*)dy, slot, gate, expert, position, kept, dgate, ntb, epoch);
+        win_of(w), w.off_yh, ctr_of(w, 1), T, d, k, (const __nv_bfloat16*)dy, slot, gate, expert,
+        position, dgate, epoch);
   else
-    p2p_combine_bwd_kernel<float><<<grid, 256, 0, st>>>(
-        win_of(w), w.off_dyr, w.off_yh, ctr_of(w, 1), T, d, E, El, k, C, Cs, (const float*)dy,
-        slot, gate, expert, position, kept, dgate, ntb, epoch);
+    p2p_combine_bwd_kernel<float><<<grid, 256, 0, st>>>(win_of(w), w.off_yh, ctr_of(w, 1), T, d, k,
+                                                        (const float*)dy, slot, gate, expert,
+                                                        position, dgate, epoch);
   MOE_LAUNCH_CHECK("p2p_combine_bwd_kernel");
   count_launch();
 }
 
-void p2p_push_home(const P2PWindow& w, uint64_t home_off, const void* src, uint32_t El,
-                   uint64_t Cs, uint32_t d, uint64_t esz, int slot, uint64_t epoch,
-                   cudaStream_t st) {
-  dim3 grid(w.P * El, (unsigned)ceil_div(Cs, 32));
-  p2p_push_kernel<<<grid, 256, 0, st>>>(win_of(w), home_off, w.off_cnt,
-                                        ctr_of(w, slot == SLOT_Y ? 2 : 3),
-                                        static_cast<const uint8_t*>(src), (int)El, Cs, d * esz,
-                                        slot, epoch);
+void p2p_push_home(const P2PWindow& w, uint64_t home_off, const void* src, int slot,
+                   uint64_t epoch, cudaStream_t st) {
+  dim3 grid(w.El * w.P, (unsigned)ceil_div(w.Cs, 64));
+  p2p_push_kernel<<<grid, 256, 0, st>>>(win_of(w), home_off, ctr_of(w, slot == SLOT_Y ? 2 : 3),
+                                        static_cast<const uint8_t*>(src), slot, epoch);
   MOE_LAUNCH_CHECK("p2p_push_kernel");
   count_launch();
 }

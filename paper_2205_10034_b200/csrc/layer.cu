@@ -115,13 +115,14 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
                "layer.exchange: must be MOE_EXCHANGE_P2P or MOE_EXCHANGE_NCCL");
   if (p2p) {
     // receive / home buffers live in one IPC window that every peer maps
-    p2p_setup(win, comm, P, rank, slot_bytes, slot_bytes, E, 0);
+    p2p_setup(win, comm, P, rank, E, Cs, (uint64_t)dm * esz, 0);
     xr = win.base + win.off_xr;
     dYr = win.base + win.off_dyr;
     Yh = win.base + win.off_yh;
     dXh = win.base + win.off_dxh;
-    cnt_recv = reinterpret_cast<int32_t*>(win.base + win.off_cnt);
   }
+  // P2P receive regions hold one contiguous group per local expert
+  ngroups = p2p ? El : P * El;
   if (!p2p) {
     xs = dalloc_bytes(owned, slot_bytes);
     xr = P > 1 ? dalloc_bytes(owned, slot_bytes) : xs;
@@ -214,7 +215,7 @@ moe_gemm_problem_t Layer::expert_problem() const {
   p.kind = MOE_GEMM_RAGGED_M;
   p.dtype_ab = dt;
   p.dtype_c = dt;
-  p.groups = P * El;
+  p.groups = ngroups;
   p.a_rows = rows;
   p.num_b = El;
   p.m = gm;
@@ -268,9 +269,12 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   // K3 (+K4 in P2P mode): dispatch into the Fusion-packed send buffer, or
   // straight into the owning ranks' receive buffers over NVLink
   if (p2p) {
-    p2p_dispatch(win, T, dm, E, El, k, C, Cs, dt, x, expert, position, kept, slot, ph, st);
+    p2p_counts(win, kept, ph, st);
+    p2p_wait(win, SLOT_CNT, ph, st);
+    p2p_dispatch(win, T, dm, k, C, dt, x, expert, position, slot, ph, st);
     mark("dispatch_p2p", st);
     p2p_wait(win, SLOT_DISPATCH, ph, st);
+    p2p_local_groups(win, gm, ga, gb, xr, st);
   } else {
     dispatch_tokens(T, dm, E, k, C, pad, dt, x, expert, position, kept, xs, slot, st);
     mark("dispatch", st);
@@ -283,7 +287,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     MOE_NCCL(ncclGroupEnd());
   }
   mark("a2a_dispatch", st);
-  build_groups(P, El, Cs, cnt_recv, gm, ga, gb, gmk, gak, gbk, st);
+  if (!p2p) build_groups(P, El, Cs, cnt_recv, gm, ga, gb, gmk, gak, gbk, st);
   // K5: H = X W1^T + b1 (stored), A = gelu(H); Y = A W2^T + b2
   {
     moe_gemm_problem_t p = expert_problem();
@@ -313,7 +317,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   }
   mark("ffn2", st);
   if (p2p) {
-    p2p_push_home(win, win.off_yh, Yl, El, Cs, dm, esz, SLOT_Y, ph, st);
+    p2p_push_home(win, win.off_yh, Yl, SLOT_Y, ph, st);
     p2p_wait(win, SLOT_Y, ph, st);
   } else if (P > 1) {
     a2a(Yl, Yh, El * Cs * dm * esz, st);
@@ -354,8 +358,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   // or straight into the owning ranks' receive buffers (P2P)
   if (p2p) {
     p2p_wait(win, SLOT_PHASE, ph - 1, st);
-    p2p_combine_bwd(win, T, dm, E, El, k, C, Cs, dt, dy, slot, gate, expert, position, kept,
-                    dgate, ph, st);
+    p2p_combine_bwd(win, T, dm, k, dt, dy, slot, gate, expert, position, dgate, ph, st);
   } else {
     combine_backward(T, dm, E, k, C, pad, dt, dy, Yh, slot, gate, kept, dYs, dgate, st);
   }
@@ -366,7 +369,10 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
                  dt == MOE_DTYPE_BF16 ? MOE_DTYPE_BF16 : MOE_DTYPE_F32,
                  dt == MOE_DTYPE_BF16 ? Epad : E, desc.has_gate_bias ? g.dbg : nullptr, st);
   mark("route_bwd", st);
-  if (p2p) p2p_wait(win, SLOT_DY, ph, st);
+  if (p2p) {
+    p2p_wait(win, SLOT_DY, ph, st);
+    p2p_local_groups(win, gm, ga, gb, dYr, st);  // zero the K-block pad rows of recv_dy
+  }
   else if (P > 1) a2a(dYs, dYr, El * Cs * dm * esz, st);
   mark("a2a_dy", st);
   // K5^T dgrad: dH = (dY W2) * gelu'(h) (stored by ffn1), db1 = column sums
@@ -400,7 +406,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("dgrad_ffn1", st);
-  if (p2p) p2p_push_home(win, win.off_dxh, dXl, El, Cs, dm, esz, SLOT_DX, ph, st);
+  if (p2p) p2p_push_home(win, win.off_dxh, dXl, SLOT_DX, ph, st);
   else if (P > 1) a2a(dXl, dXh, El * Cs * dm * esz, st);
   mark("a2a_dx", st);
   // K5^T wgrad: dW1[j] = sum dH^T X, dW2[j] = sum dY^T A (RAGGED_K over slices)
@@ -411,12 +417,12 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.epilogue = MOE_EPI_STORE;
     p.dtype_ab = dt;
     p.dtype_c = MOE_DTYPE_F32;
-    p.groups = P * El;
+    p.groups = ngroups;
     p.a_rows = rows;
     p.num_b = El;
-    p.m = gmk;
-    p.a_row = gak;
-    p.b = gbk;
+    p.m = p2p ? gm : gmk;
+    p.a_row = p2p ? ga : gak;
+    p.b = p2p ? gb : gbk;
     p.M = dff;
     p.N = dm;
     p.A = dH;
@@ -434,7 +440,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
     mark("wgrad_w2", st);
   }
-  group_colsum(P * El, gm, ga, gb, El, dm, dt, dYr, g.db2, st, Cs);
+  group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs);
   mark("bias_grads", st);
   if (p2p) p2p_wait(win, SLOT_DX, ph, st);
   // gate dgrad with the combine backward folded into its epilogue:

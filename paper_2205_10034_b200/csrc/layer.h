@@ -44,6 +44,7 @@ struct Layer {
   bool p2p = false;       // EP exchange over NVLink peer memory
   P2PWindow win;
   uint64_t phase = 0;     // forward/backward phase counter (P2P epochs)
+  uint32_t ngroups = 1;   // expert GEMM groups: P*El slices, or El experts (P2P)
 
   std::vector<void*> owned;
   // routing state
