@@ -36,13 +36,18 @@ constexpr int EPI_WARPS = 8;
 constexpr int MAX_GROUPS = 1024;
 constexpr int STG = 2048;  // one 32-row x 64B staging tile
 
-template <int BN, int EPI, bool CF32>
+// CG = CTAs per MMA (cta_group): CG == 2 pairs two SMs on a 256 x BN tile,
+// each CTA holding its 128 A rows and BN/2 B columns (halves the per-SM smem
+// operand traffic of the 128 x 256 single-CTA MMA).
+template <int BN, int EPI, bool CF32, int CG>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int EPI_HEAVY = (EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU) ? 1 : 0;
   static constexpr int STAGES =
-      (BN == 256) ? ((EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU) ? 3 : 4) : (BN == 128 ? 6 : 8);
+      (CG == 2) ? (EPI_HEAVY ? 5 : 6)
+                : ((BN == 256) ? (EPI_HEAVY ? 3 : 4) : (BN == 128 ? 6 : 8));
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int CW = CF32 ? 16 : 32;  // epilogue chunk width (columns): 64B per row
   static constexpr int NOUT = (EPI == MOE_EPI_GELU) ? 2 : 1;
@@ -155,12 +160,16 @@ __device__ __forceinline__ void store_row_direct(void* base, long long off, int 
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32>
+template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32, int CG>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                    const __grid_constant__ CUtensorMap tmAux, const Args args) {
-  using C_ = Cfg<BN, EPI, CF32>;
+  using C_ = Cfg<BN, EPI, CF32, CG>;
+  constexpr int TM = BM * CG;  // tile rows per work item (the CTA pair)
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // 0 = leader
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   constexpr int CW = C_::CW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -190,20 +199,21 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS);
+      mbar_init(&tempty[a], EPI_WARPS * CG);  // leader's counts both CTAs' epilogues
     }
     for (int a = 0; a < 2 * EPI_WARPS; ++a) mbar_init(&abar[a], 1);
     fence_mbar_init();
   }
   if (warp == 2) {
-    tmem_alloc(tmem_hold, C_::TMEM_COLS);
+    if (CG == 2) tmem_alloc_2sm(tmem_hold, C_::TMEM_COLS);
+    else tmem_alloc(tmem_hold, C_::TMEM_COLS);
     tc_fence_before();
   }
   int* scratch = reinterpret_cast<int*>(smem);  // stage 0 is free during setup
   if (KIND == 0) {
     for (int g = threadIdx.x; g < G; g += THREADS) {
       const int m = args.gm[g];
-      scratch[g] = ((m + BM - 1) / BM) * nblk_n;
+      scratch[g] = ((m + TM - 1) / TM) * nblk_n;
     }
   } else {
     for (int g = threadIdx.x; g < G; g += THREADS) {
@@ -226,11 +236,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // peer barriers initialised before any TMA signals them
   tc_fence_after();
   const uint32_t tmem_base = *tmem_hold;
 
   int total_work;
-  const int mt = args.M / BM;  // RAGGED_K only
+  const int mt = args.M / TM;  // RAGGED_K only
   if (KIND == 0) total_work = tab[G];
   else total_work = tab[MAX_GROUPS] * mt * nblk_n;
 
@@ -260,35 +271,50 @@ __global__ void __launch_bounds__(THREADS, 1)
     return n;
   };
 
-  constexpr uint32_t IDESC = umma_idesc_bf16(BM, BN, A_MN, B_MN);
+  constexpr uint32_t IDESC = umma_idesc_bf16(TM, BN, A_MN, B_MN);
+  constexpr int BH = BN / CG;  // B columns held by this CTA
 
   if (warp == 0) {
     // ================= TMA producer =================
+    // CG == 2: this CTA loads its 128 A rows and BN/2 B columns; all bytes
+    // complete on the LEADER's full barrier, which only the leader arms.
     if (lane == 0) {
+      const uint32_t full0 = smem_u32(&full[0]);
       uint32_t it = 0;
-      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+      for (int w = unit; w < total_work; w += nunits) {
         int g, mb, nb;
         decode(w, g, mb, nb);
+        auto load = [&](void* dst, const CUtensorMap* m, int s, int c0, int c1) {
+          if (CG == 2)
+            tma_load_2d_2sm(dst, m, mapa_shared(full0 + s * 8, 0), c0, c1);
+          else
+            tma_load_2d(dst, m, &full[s], c0, c1);
+        };
+        auto arm = [&](int s) {
+          if (crank == 0) mbar_arrive_expect_tx(&full[s], C_::STAGE_BYTES * CG);
+        };
         if (KIND == 0) {
-          const int arow = args.ga[g] + mb * BM;
+          const int arow = args.ga[g] + mb * TM + (int)crank * BM;
           const int brow = args.gb[g] * (B_MN ? args.K : args.N);
+          const int bcol = nb * BN + (int)crank * BH;
           const int nkb = args.K / BK;
           for (int kb = 0; kb < nkb; ++kb, ++it) {
             const int s = it % C_::STAGES;
             mbar_wait(&empty[s], ((it / C_::STAGES) & 1) ^ 1);
             uint8_t* sA = smem + s * C_::STAGE_BYTES;
             uint8_t* sB = sA + C_::A_BYTES;
-            mbar_arrive_expect_tx(&full[s], C_::STAGE_BYTES);
-            tma_load_2d(sA, &tmA, &full[s], kb * BK, arow);  // A K-major box {64,128}
+            arm(s);
+            load(sA, &tmA, s, kb * BK, arow);  // A K-major box {64,128}
             if (!B_MN) {
-              tma_load_2d(sB, &tmB, &full[s], kb * BK, brow + nb * BN);
+              load(sB, &tmB, s, kb * BK, brow + bcol);
             } else {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_2d(sB + j * 8192, &tmB, &full[s], nb * BN + j * 64, brow + kb * BK);
+              for (int j = 0; j < BH / 64; ++j) load(sB + j * 8192, &tmB, s, bcol + j * 64, brow + kb * BK);
             }
           }
         } else {
+          const int acol = mb * TM + (int)crank * BM;
+          const int bcol = nb * BN + (int)crank * BH;
           for (int q = tab[g]; q < tab[g + 1]; ++q) {
             const int rows = args.gm[q];
             const int r0 = args.ga[q];
@@ -297,24 +323,22 @@ __global__ void __launch_bounds__(THREADS, 1)
               mbar_wait(&empty[s], ((it / C_::STAGES) & 1) ^ 1);
               uint8_t* sA = smem + s * C_::STAGE_BYTES;
               uint8_t* sB = sA + C_::A_BYTES;
-              mbar_arrive_expect_tx(&full[s], C_::STAGE_BYTES);
+              arm(s);
               const int row = r0 + kb * BK;
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j)
-                tma_load_2d(sA + j * 8192, &tmA, &full[s], mb * BM + j * 64, row);
+              for (int j = 0; j < BM / 64; ++j) load(sA + j * 8192, &tmA, s, acol + j * 64, row);
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                tma_load_2d(sB + j * 8192, &tmB, &full[s], nb * BN + j * 64, row);
+              for (int j = 0; j < BH / 64; ++j) load(sB + j * 8192, &tmB, s, bcol + j * 64, row);
             }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
+    // ================= MMA issuer (leader CTA only when paired) =================
+    if (lane == 0 && crank == 0) {
       uint32_t it = 0, tcount = 0;
-      for (int w = blockIdx.x; w < total_work; w += gridDim.x, ++tcount) {
+      for (int w = unit; w < total_work; w += nunits, ++tcount) {
         int g, mb, nb;
         decode(w, g, mb, nb);
         const int nkb = num_kblocks(g);
@@ -334,11 +358,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      : umma_desc_sw128(aBase + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? umma_desc_sw128(bBase + kk * 2048, 8192, 1024)
                                      : umma_desc_sw128(bBase + kk * 32, 16, 1024);
-            tc_mma_bf16(d_tmem, da, db, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            if (CG == 2) tc_mma_bf16_2sm(d_tmem, da, db, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            else tc_mma_bf16(d_tmem, da, db, IDESC, (kb | kk) != 0 ? 1u : 0u);
           }
-          tc_commit(&empty[s]);
+          if (CG == 2) tc_commit_2sm_mc(&empty[s], 0x3);
+          else tc_commit(&empty[s]);
         }
-        tc_commit(&tfull[acc]);
+        if (CG == 2) tc_commit_2sm_mc(&tfull[acc], 0x3);
+        else tc_commit(&tfull[acc]);
       }
     }
   } else if (warp >= 4) {
@@ -354,10 +381,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* ab = abar + 2 * ew;
     uint32_t aph[2] = {0, 0};
     uint32_t tcount = 0;
-    for (int w = blockIdx.x; w < total_work; w += gridDim.x, ++tcount) {
+    const uint32_t tempty0 = smem_u32(&tempty[0]);
+    for (int w = unit; w < total_work; w += nunits, ++tcount) {
       int g, mb, nb;
       decode(w, g, mb, nb);
-      const int row0 = mb * BM + q * 32;  // first tile row of this warp
+      const int row0 = mb * TM + (int)crank * BM + q * 32;  // first tile row of this warp
       int nvalid, bidx;
       long long orow0;
       if (KIND == 0) {
@@ -502,15 +530,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (CG == 2) mbar_arrive_cluster(mapa_shared(tempty0 + acc * 8, 0));
+        else mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) bulk_wait0();
   }
 
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // the leader's MMAs into our TMEM are long complete
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, C_::TMEM_COLS);
+    if (CG == 2) tmem_dealloc_2sm(tmem_base, C_::TMEM_COLS);
+    else tmem_dealloc(tmem_base, C_::TMEM_COLS);
   }
 }
 
@@ -558,10 +591,11 @@ static CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, ui
   return m;
 }
 
-template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32>
+template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32, int CG = 1>
 static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
-  using C_ = Cfg<BN, EPI, CF32>;
-  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, KIND, EPI, CF32>;
+  using C_ = Cfg<BN, EPI, CF32, CG>;
+  constexpr int BH = BN / CG;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, KIND, EPI, CF32, CG>;
   static bool attr = false;
   if (!attr) {
     MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
@@ -574,7 +608,7 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
     if (!B_MN) {
       const uint64_t ldb = p.ldb ? p.ldb : p.K;
       const uint64_t rows = p.b_rows ? p.b_rows : (uint64_t)p.num_b * p.N;
-      tb = make_map(p.B, p.K, rows, ldb, 64, BN);
+      tb = make_map(p.B, p.K, rows, ldb, 64, BH);
     } else {
       const uint64_t ldb = p.ldb ? p.ldb : p.N;
       const uint64_t rows = p.b_rows ? p.b_rows : (uint64_t)p.num_b * p.K;
@@ -614,8 +648,23 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
   a.ldc = (long long)p.ldc;
   a.transpose_c = p.transpose_c;
   a.num_b = (int)p.num_b;
-  const int grid = num_sms();
-  kern<<<grid, THREADS, C_::SMEM, st>>>(ta, tb, tcm, tc2, tax, a);
+  if (CG == 1) {
+    kern<<<num_sms(), THREADS, C_::SMEM, st>>>(ta, tb, tcm, tc2, tax, a);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(num_sms() & ~1));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    MOE_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tc2, tax, a));
+  }
   MOE_LAUNCH_CHECK("tc_gemm_kernel");
   count_launch();
 }
@@ -640,26 +689,26 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
     switch (p.epilogue) {
       case MOE_EPI_STORE:
         if (bmn) {
-          if (f32) launch<256, false, true, 0, MOE_EPI_STORE, true>(p, st);
-          else launch<256, false, true, 0, MOE_EPI_STORE, false>(p, st);
+          if (f32) launch<256, false, true, 0, MOE_EPI_STORE, true, 2>(p, st);
+          else launch<256, false, true, 0, MOE_EPI_STORE, false, 2>(p, st);
         } else {
-          if (f32) launch<256, false, false, 0, MOE_EPI_STORE, true>(p, st);
-          else launch<256, false, false, 0, MOE_EPI_STORE, false>(p, st);
+          if (f32) launch<256, false, false, 0, MOE_EPI_STORE, true, 2>(p, st);
+          else launch<256, false, false, 0, MOE_EPI_STORE, false, 2>(p, st);
         }
         return;
       case MOE_EPI_GELU:
         arg_check(!bmn && !f32, "gemm.epilogue: GELU needs K-major B and bf16 C");
-        launch<256, false, false, 0, MOE_EPI_GELU, false>(p, st);
+        launch<256, false, false, 0, MOE_EPI_GELU, false, 2>(p, st);
         return;
       case MOE_EPI_DGELU:
         arg_check(bmn && !f32, "gemm.epilogue: DGELU needs MN-major B and bf16 C");
-        launch<256, false, true, 0, MOE_EPI_DGELU, false>(p, st);
+        launch<256, false, true, 0, MOE_EPI_DGELU, false, 2>(p, st);
         return;
       case MOE_EPI_GATHER_ADD:
         arg_check(bmn && !f32 && p.gather_src && p.gather_idx && p.gather_k >= 1 &&
                       p.gather_k <= 2,
                   "gemm.epilogue: GATHER_ADD needs MN-major B, bf16 C, gather_src/idx, k<=2");
-        launch<256, false, true, 0, MOE_EPI_GATHER_ADD, false>(p, st);
+        launch<256, false, true, 0, MOE_EPI_GATHER_ADD, false, 2>(p, st);
         return;
       default:
         fail(MOE_ERR_INVALID_ARGUMENT, "gemm.epilogue: unsupported for RAGGED_M");
@@ -675,7 +724,8 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
     }
     arg_check(p.epilogue == MOE_EPI_STORE && !p.transpose_c,
               "gemm.epilogue: RAGGED_K supports STORE or ATOMIC_ADD");
-    launch<256, true, true, 1, MOE_EPI_STORE, true>(p, st);
+    if (p.M % 256 == 0) launch<256, true, true, 1, MOE_EPI_STORE, true, 2>(p, st);
+    else launch<256, true, true, 1, MOE_EPI_STORE, true, 1>(p, st);
   }
 }
 
