@@ -461,12 +461,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         float f2[CW];
         if (EPI == MOE_EPI_GELU) {
 #pragma unroll
-          for (int i = 0; i < CW; ++i) {
-            const float h = f[i];
-            const float e = erff(h * 0.70710678118654752440f);
-            f[i] = 0.5f * h * (1.0f + e);
-            f2[i] = 0.5f * (1.0f + e) + h * 0.39894228040143267794f * __expf(-0.5f * h * h);
-          }
+          for (int i = 0; i < CW; ++i) gelu_and_grad_fast(f[i], f[i], f2[i]);
         }
         if (EPI == MOE_EPI_DGELU) {
           const uint8_t* ax = auxb + (c & 1) * STG;
