@@ -343,6 +343,31 @@ def main():
                          "oracle/moe_oracle.c fp64-accumulate, OpenMP)"}
 
     a2a_ms = sum(v for n, v in phase_tot.items() if ".a2a" in n) / args.steps
+    nvlink = None
+    if ws > 1:
+        # token rows that cross NVLink per exchange per GPU: kept rows owned by
+        # other ranks (uniform routing: (P-1)/P of them), d * 2 bytes each
+        row_bytes = d * (2 if dtype == torch.bfloat16 else 4)
+        xbytes = kept_local * row_bytes * (ws - 1) / ws
+        ph = {n: v / args.steps for n, v in phase_tot.items()}
+        if args.exchange == "p2p":
+            ex = {"dispatch": ph.get("fwd.dispatch_p2p", 0) + ph.get("fwd.a2a_dispatch", 0),
+                  "combine": ph.get("fwd.a2a_combine", 0),
+                  "dy": ph.get("bwd.combine_bwd", 0) + ph.get("bwd.a2a_dy", 0),
+                  "dx": ph.get("bwd.a2a_dx", 0)}
+        else:
+            ex = {"dispatch": ph.get("fwd.a2a_dispatch", 0), "combine": ph.get("fwd.a2a_combine", 0),
+                  "dy": ph.get("bwd.a2a_dy", 0), "dx": ph.get("bwd.a2a_dx", 0)}
+        ex_ms = sum(ex.values())
+        ach = 4 * xbytes / (ex_ms / 1000.0) / 1e9 if ex_ms > 0 else None
+        nvlink = {"bound": "nvlink", "unit": "GB/s", "achieved": ach,
+                  "peak": 770.0, "peak_source": "measured peer copy per direction "
+                  "(B200_PROFILING.md; 900 nominal)",
+                  "frac": ach / 770.0 if ach else None,
+                  "bytes_per_exchange_per_gpu": xbytes, "exchanges_per_step": 4,
+                  "exchange_ms": ex,
+                  "note": "p2p phases include the fused dispatch/combine-bwd kernel work"
+                  if args.exchange == "p2p" else "ncclAlltoAll of capacity-padded buffers"}
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
@@ -358,6 +383,7 @@ def main():
         "clocks": clocks,
         "routing": {"imbalance_ratio": imb, "drop_rate": drop},
         "a2a_ms_per_step": a2a_ms if ws > 1 else 0.0,
+        "nvlink": nvlink,
         "phases_ms_per_step": {n: v / args.steps for n, v in sorted(phase_tot.items())},
     }
     if rank == 0:
