@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -79,6 +80,16 @@ struct Args {
   long long ldc;
   int transpose_c;
   int num_b;
+};
+
+// Per-peer destinations of the remote-store epilogue (RemoteRows on device).
+struct RemoteOut {
+  CUtensorMap maps[8];  // [P] bf16 [E*Cs][N] views of each peer's destination buffer
+  uint8_t** peers;
+  unsigned long long home_off;
+  const int* cnt;
+  int P, me, E, El;
+  long long Cs;
 };
 
 // Exclusive scan of vals[0..n) (smem) into out[0..n] by one warp.
@@ -160,11 +171,12 @@ __device__ __forceinline__ void store_row_direct(void* base, long long off, int 
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32, int CG>
+template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32, int CG, bool REMOTE>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
-                   const __grid_constant__ CUtensorMap tmAux, const Args args) {
+                   const __grid_constant__ CUtensorMap tmAux, const Args args,
+                   const __grid_constant__ RemoteOut ro) {
   using C_ = Cfg<BN, EPI, CF32, CG>;
   constexpr int TM = BM * CG;  // tile rows per work item (the CTA pair)
   const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // 0 = leader
@@ -397,6 +409,30 @@ __global__ void __launch_bounds__(THREADS, 1)
         bidx = args.gb[tab[g]];
         orow0 = (long long)bidx * args.M + row0;
       }
+      // REMOTE: lane s holds the exclusive row offset of source s inside this
+      // expert's contiguous receive region
+      int rexcl = 0, rexp = 0;
+      if (REMOTE) {
+        rexp = ro.me * ro.El + bidx;
+        const int cv = lane < ro.P ? ro.cnt[lane * ro.E + rexp] : 0;
+        int incl = cv;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += u;
+        }
+        rexcl = incl - cv;
+      }
+      // source rank of group row r (warp-collective: every lane must call it)
+      auto src_of = [&](int r) {
+        int sidx = 0;
+#pragma unroll
+        for (int qq = 1; qq < 8; ++qq) {
+          const int oq = __shfl_sync(0xffffffffu, rexcl, qq);
+          if (qq < ro.P && r >= oq) sidx = qq;
+        }
+        return sidx;
+      };
       const int col_base = nb * BN + half * HALF;
       if (EPI == MOE_EPI_DGELU && lane == 0 && col_base < args.N) {
         mbar_arrive_expect_tx(&ab[0], STG);
@@ -488,6 +524,31 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
           }
         }
+        if (REMOTE) {
+          // return all-to-all fused into the epilogue: rows go straight to the
+          // source rank's buffer over NVLink
+          const int sl = src_of(row0 + lane);                    // this lane's row
+          const int offl = __shfl_sync(0xffffffffu, rexcl, sl);
+          const int s0 = __shfl_sync(0xffffffffu, sl, 0);
+          const int s1 = __shfl_sync(0xffffffffu, sl, max(nvalid - 1, 0));
+          const int off0 = __shfl_sync(0xffffffffu, rexcl, s0);
+          if (full_tile && s0 == s1) {
+            if (lane == 0) bulk_wait_read0();
+            __syncwarp();
+            stage_row<CF32>(stg, lane, f);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&ro.maps[s0], stg, n0, (int)(rexp * ro.Cs + row0 - off0));
+              bulk_commit();
+            }
+          } else if (row_ok) {
+            uint8_t* dst = ro.peers[sl] + ro.home_off;
+            store_row_direct<CF32>(dst, (rexp * ro.Cs + row0 + lane - offl) * args.ldc + n0,
+                                   ncols, f);
+          }
+          continue;
+        }
         const bool want_colsum = EPI == MOE_EPI_DGELU && args.colsum != nullptr;
         if (full_tile || want_colsum) {
           if (lane == 0) bulk_wait_read0();  // previous store out of this buffer is done
@@ -531,6 +592,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     if (lane == 0) bulk_wait0();
+    if (REMOTE) __threadfence_system();  // remote rows visible before the signal kernel
   }
 
   __syncthreads();
@@ -586,11 +648,13 @@ static CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, ui
   return m;
 }
 
-template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32, int CG = 1>
-static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
+template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32, int CG = 1,
+          bool REMOTE = false>
+static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
+                   const RemoteRows* remote = nullptr) {
   using C_ = Cfg<BN, EPI, CF32, CG>;
   constexpr int BH = BN / CG;
-  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, KIND, EPI, CF32, CG>;
+  auto kern = tc_gemm_kernel<BN, A_MN, B_MN, KIND, EPI, CF32, CG, REMOTE>;
   static bool attr = false;
   if (!attr) {
     MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
@@ -643,8 +707,25 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
   a.ldc = (long long)p.ldc;
   a.transpose_c = p.transpose_c;
   a.num_b = (int)p.num_b;
+  static RemoteOut ro;  // host staging of the remote descriptor (copied into the launch)
+  std::memset(&ro, 0, sizeof(ro));
+  if (REMOTE) {
+    require(remote != nullptr && remote->P <= 8, MOE_ERR_LOGIC, "gemm: remote rows descriptor");
+    for (uint32_t q = 0; q < remote->P; ++q)
+      ro.maps[q] = make_map(remote->peers_host[q] + remote->home_off, p.N,
+                            (uint64_t)remote->E * remote->Cs, p.ldc, C_::CW, 32, CF32,
+                            CU_TENSOR_MAP_SWIZZLE_64B);
+    ro.peers = remote->peers_dev;
+    ro.home_off = remote->home_off;
+    ro.cnt = remote->cnt;
+    ro.P = (int)remote->P;
+    ro.me = (int)remote->me;
+    ro.E = (int)remote->E;
+    ro.El = (int)remote->El;
+    ro.Cs = (long long)remote->Cs;
+  }
   if (CG == 1) {
-    kern<<<num_sms(), THREADS, C_::SMEM, st>>>(ta, tb, tcm, tc2, tax, a);
+    kern<<<num_sms(), THREADS, C_::SMEM, st>>>(ta, tb, tcm, tc2, tax, a, ro);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(num_sms() & ~1));
@@ -658,7 +739,7 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    MOE_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tc2, tax, a));
+    MOE_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tc2, tax, a, ro));
   }
   MOE_LAUNCH_CHECK("tc_gemm_kernel");
   count_launch();
@@ -666,8 +747,16 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st) {
 
 }  // namespace tc
 
-void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
+void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st, const RemoteRows* remote) {
   using namespace tc;
+  if (remote != nullptr) {
+    arg_check(p.kind == MOE_GEMM_RAGGED_M && p.epilogue == MOE_EPI_STORE &&
+                  p.dtype_c == MOE_DTYPE_BF16,
+              "gemm.remote: only bf16 RAGGED_M STORE GEMMs write to peers");
+    if (p.b_mn_major) launch<256, false, true, 0, MOE_EPI_STORE, false, 2, true>(p, st, remote);
+    else launch<256, false, false, 0, MOE_EPI_STORE, false, 2, true>(p, st, remote);
+    return;
+  }
   arg_check(p.groups >= 1 && p.groups <= MAX_GROUPS, "gemm.groups: must be in [1, 1024]");
   arg_check(p.dtype_ab == MOE_DTYPE_BF16, "gemm.dtype_ab: tcgen05 path needs bf16");
   const bool f32 = p.dtype_c == MOE_DTYPE_F32;

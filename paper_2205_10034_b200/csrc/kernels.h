@@ -13,11 +13,27 @@ namespace moe {
 // Kernel launch accounting (moe_kernel_launch_count).
 void count_launch(uint64_t n = 1);
 
+// Remote row destinations for expert parallelism over peer memory: output row
+// r of local expert group j came from source s (rows [off_s, off_s + cnt[s][e])
+// of the group, e = me*El + j) and is stored straight into rank s's buffer at
+// window offset `home_off`, row e*Cs + (r - off_s) — the GEMM epilogue performs
+// the return all-to-all tile by tile.
+struct RemoteRows {
+  uint8_t* const* peers_host;  // [P] window bases (host copies, for tensor maps)
+  uint8_t** peers_dev;         // [P] window bases (device array)
+  uint64_t home_off;
+  const int32_t* cnt;          // device [P][E] kept counts
+  uint32_t P, me, E, El;
+  uint64_t Cs;
+};
+
 // K5: grouped GEMM. bf16 -> tcgen05 (gemm_tc.cu), fp32 -> SIMT FFMA (gemm_simt.cu).
-void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st);
+void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st,
+                     const RemoteRows* remote = nullptr);
 void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st);
-inline void grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
-  if (p.dtype_ab == MOE_DTYPE_BF16) tc_grouped_gemm(p, st);
+inline void grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st,
+                         const RemoteRows* remote = nullptr) {
+  if (p.dtype_ab == MOE_DTYPE_BF16) tc_grouped_gemm(p, st, remote);
   else simt_grouped_gemm(p, st);
 }
 

@@ -209,6 +209,20 @@ void Layer::a2a(const void* send, void* recv, uint64_t bytes_per_peer, cudaStrea
   MOE_NCCL(ncclAlltoAll(send, recv, bytes_per_peer, ncclUint8, (ncclComm_t)comm, st));
 }
 
+RemoteRows Layer::remote_rows(uint64_t home_off) const {
+  RemoteRows r;
+  r.peers_host = win.peer_host;
+  r.peers_dev = win.peer_dev;
+  r.home_off = home_off;
+  r.cnt = reinterpret_cast<const int32_t*>(win.base + win.off_cnt);
+  r.P = P;
+  r.me = rank;
+  r.E = E;
+  r.El = El;
+  r.Cs = Cs;
+  return r;
+}
+
 moe_gemm_problem_t Layer::expert_problem() const {
   moe_gemm_problem_t p;
   std::memset(&p, 0, sizeof(p));
@@ -303,6 +317,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     grouped_gemm(p, st);
   }
   mark("ffn1", st);
+  const bool fused_return = p2p && dt == MOE_DTYPE_BF16;
   {
     moe_gemm_problem_t p = expert_problem();
     p.epilogue = MOE_EPI_STORE;
@@ -313,11 +328,18 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     p.C = Yl;
     p.bias = w.b2;
     p.ldc = dm;
-    grouped_gemm(p, st);
+    if (fused_return) {
+      // the epilogue stores Y rows straight into the source ranks' home buffers
+      const RemoteRows rr = remote_rows(win.off_yh);
+      grouped_gemm(p, st, &rr);
+    } else {
+      grouped_gemm(p, st);
+    }
   }
   mark("ffn2", st);
   if (p2p) {
-    p2p_push_home(win, win.off_yh, Yl, SLOT_Y, ph, st);
+    if (fused_return) p2p_signal(win, SLOT_Y, ph, st);
+    else p2p_push_home(win, win.off_yh, Yl, SLOT_Y, ph, st);
     p2p_wait(win, SLOT_Y, ph, st);
   } else if (P > 1) {
     a2a(Yl, Yh, El * Cs * dm * esz, st);
@@ -393,6 +415,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("dgrad_ffn2", st);
+  const bool fused_return = p2p && dt == MOE_DTYPE_BF16;
   {
     moe_gemm_problem_t p = expert_problem();
     p.epilogue = MOE_EPI_STORE;
@@ -403,10 +426,18 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.B = w.w1;
     p.C = dXl;
     p.ldc = dm;
-    grouped_gemm(p, st);
+    if (fused_return) {
+      const RemoteRows rr = remote_rows(win.off_dxh);  // dX rows straight to their sources
+      grouped_gemm(p, st, &rr);
+    } else {
+      grouped_gemm(p, st);
+    }
   }
   mark("dgrad_ffn1", st);
-  if (p2p) p2p_push_home(win, win.off_dxh, dXl, SLOT_DX, ph, st);
+  if (p2p) {
+    if (fused_return) p2p_signal(win, SLOT_DX, ph, st);
+    else p2p_push_home(win, win.off_dxh, dXl, SLOT_DX, ph, st);
+  }
   else if (P > 1) a2a(dXl, dXh, El * Cs * dm * esz, st);
   mark("a2a_dx", st);
   // K5^T wgrad: dW1[j] = sum dH^T X, dW2[j] = sum dY^T A (RAGGED_K over slices)

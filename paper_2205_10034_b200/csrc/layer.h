@@ -30,6 +30,7 @@ struct Layer {
                        cudaStream_t st);
 
   moe_gemm_problem_t expert_problem() const;
+  RemoteRows remote_rows(uint64_t home_off) const;
   void a2a(const void* send, void* recv, uint64_t bytes_per_peer, cudaStream_t st);
   void mark(const char* name, cudaStream_t st);
 
