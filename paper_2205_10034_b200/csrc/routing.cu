@@ -26,23 +26,6 @@ constexpr int CHUNK = 256;  // tokens per routing block (8 warps x 32)
 constexpr int RT_THREADS = 256;
 constexpr int MAX_E = 256;
 
-struct Best {
-  float v;
-  int i;
-};
-__device__ __forceinline__ bool better(const Best& a, const Best& b) {
-  return a.v > b.v || (a.v == b.v && a.i < b.i);
-}
-__device__ __forceinline__ Best warp_best(Best b) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    Best c;
-    c.v = __shfl_xor_sync(0xffffffffu, b.v, o);
-    c.i = __shfl_xor_sync(0xffffffffu, b.i, o);
-    if (better(c, b)) b = c;
-  }
-  return b;
-}
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -50,100 +33,115 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 __device__ __forceinline__ float nan_to_ninf(float v) { return isnan(v) ? -INFINITY : v; }
 
-// Phase A: per token top-k + softmax; per chunk: histograms (expert-major
-// [i][E][nchunks]), in-chunk ranks, softmax column partial sums.
+// Phase A: thread per token (the block is one 256-token chunk): top-k on the
+// fp32 logits, softmax, gates; per chunk: histograms (expert-major
+// [i][E][nchunks]), in-chunk ranks (warp match over 32 consecutive tokens +
+// per-warp histograms), and softmax column partial sums reduced in a fixed
+// order (deterministic aux loss).
 __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
     uint64_t T, int E, int k, const float* __restrict__ logits, int32_t* __restrict__ expert,
     float* __restrict__ gate, int32_t* __restrict__ rank_local, int32_t* __restrict__ chunk_cnt,
     float* __restrict__ psum_part, uint64_t nchunks) {
   __shared__ int hist[2][8][MAX_E];
   __shared__ float pw[8][MAX_E];
-  __shared__ int ech[2][CHUNK];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t chunk = blockIdx.x;
-  const uint64_t t0 = chunk * CHUNK;
+  const uint64_t t = chunk * CHUNK + threadIdx.x;
+  const bool valid = t < T;
 
   for (int i = threadIdx.x; i < 2 * 8 * MAX_E; i += RT_THREADS) (&hist[0][0][0])[i] = 0;
-  float pacc[MAX_E / 32];
-#pragma unroll
-  for (int j = 0; j < MAX_E / 32; ++j) pacc[j] = 0.f;
 
-  for (int tt = 0; tt < 32; ++tt) {
-    const int local = warp * 32 + tt;
-    const uint64_t t = t0 + local;
-    if (t >= T) {
-      if (lane == 0) { ech[0][local] = -1; ech[1][local] = -1; }
-      continue;
+  // pass 1: top-1 / top-2 on logits (NaN read as -inf, ties to the lowest index)
+  const float4* L4 = reinterpret_cast<const float4*>(logits + t * E);
+  const float* L = logits + t * E;
+  float v1 = -INFINITY, v2 = -INFINITY;
+  int i1 = 0x7fffffff, i2 = 0x7fffffff;
+  auto consider = [&](float v, int e) {
+    v = nan_to_ninf(v);
+    if (v > v1 || (v == v1 && e < i1)) {
+      v2 = v1; i2 = i1; v1 = v; i1 = e;
+    } else if (v > v2 || (v == v2 && e < i2)) {
+      v2 = v; i2 = e;
     }
-    const float* L = logits + t * E;
-    // lane-local top-2 over e = lane + 32 j
-    Best b1{-INFINITY, 0x7fffffff}, b2{-INFINITY, 0x7fffffff};
-    float lv[MAX_E / 32];
-#pragma unroll
-    for (int j = 0; j < MAX_E / 32; ++j) {
-      const int e = lane + 32 * j;
-      lv[j] = -INFINITY;
-      if (e < E) {
-        lv[j] = nan_to_ninf(L[e]);
-        Best c{lv[j], e};
-        if (better(c, b1)) { b2 = b1; b1 = c; }
-        else if (better(c, b2)) b2 = c;
+  };
+  const bool vec = (E % 4) == 0;
+  if (valid) {
+    if (vec) {
+      for (int q = 0; q < E / 4; ++q) {
+        const float4 f = __ldg(L4 + q);
+        consider(f.x, 4 * q);
+        consider(f.y, 4 * q + 1);
+        consider(f.z, 4 * q + 2);
+        consider(f.w, 4 * q + 3);
       }
-    }
-    const Best w1 = warp_best(b1);
-    Best w2{-INFINITY, 0x7fffffff};
-    if (k == 2) {
-      const Best cand = (b1.i == w1.i) ? b2 : b1;
-      w2 = warp_best(cand);
-    }
-    const float m = w1.v;
-    float z = 0.f;
-    float ex[MAX_E / 32];
-#pragma unroll
-    for (int j = 0; j < MAX_E / 32; ++j) {
-      const int e = lane + 32 * j;
-      ex[j] = (e < E) ? expf(lv[j] - m) : 0.f;
-      z += ex[j];
-    }
-    z = warp_sum(z);
-    const float inv = 1.0f / z;
-#pragma unroll
-    for (int j = 0; j < MAX_E / 32; ++j) pacc[j] += ex[j] * inv;
-    if (lane == 0) {
-      if (k == 1) {
-        expert[t] = w1.i;
-        gate[t] = inv;  // p[e1] = exp(0) / z
-      } else {
-        const float p2 = expf(w2.v - m);
-        const float s = 1.0f + p2;
-        expert[2 * t] = w1.i;
-        expert[2 * t + 1] = w2.i;
-        gate[2 * t] = 1.0f / s;
-        gate[2 * t + 1] = p2 / s;
-      }
-      ech[0][local] = w1.i;
-      ech[1][local] = (k == 2) ? w2.i : -1;
+    } else {
+      for (int e = 0; e < E; ++e) consider(__ldg(L + e), e);
     }
   }
+  // pass 2: softmax denominator (max = v1)
+  float z = 0.f;
+  if (valid) {
+    if (vec) {
+      for (int q = 0; q < E / 4; ++q) {
+        const float4 f = __ldg(L4 + q);
+        z += expf(nan_to_ninf(f.x) - v1) + expf(nan_to_ninf(f.y) - v1) +
+             expf(nan_to_ninf(f.z) - v1) + expf(nan_to_ninf(f.w) - v1);
+      }
+    } else {
+      for (int e = 0; e < E; ++e) z += expf(nan_to_ninf(__ldg(L + e)) - v1);
+    }
+  }
+  const float inv = valid ? 1.0f / z : 0.f;
+  if (valid) {
+    if (k == 1) {
+      expert[t] = i1;
+      gate[t] = inv;  // p[e1] = exp(0) / z
+    } else {
+      const float p2 = expf(v2 - v1);
+      const float sden = 1.0f + p2;
+      expert[2 * t] = i1;
+      expert[2 * t + 1] = i2;
+      gate[2 * t] = 1.0f / sden;
+      gate[2 * t + 1] = p2 / sden;
+    }
+  }
+  // pass 3: softmax column sums over the warp's 32 tokens: lane l owns experts
+  // l, l+32, ...; token j's (max, 1/z) broadcast from lane j; rows read
+  // coalesced.  Then a fixed-order sum over the 8 warps (deterministic aux).
+  {
+    float acc[MAX_E / 32];
 #pragma unroll
-  for (int j = 0; j < MAX_E / 32; ++j) {
-    const int e = lane + 32 * j;
-    if (e < E) pw[warp][e] = pacc[j];
+    for (int q = 0; q < MAX_E / 32; ++q) acc[q] = 0.f;
+    const uint64_t t0w = chunk * CHUNK + warp * 32;
+    for (int j = 0; j < 32; ++j) {
+      const float mj = __shfl_sync(0xffffffffu, v1, j);
+      const float ij = __shfl_sync(0xffffffffu, inv, j);
+      if (t0w + j >= T) break;
+      const float* Lj = logits + (t0w + j) * E;
+#pragma unroll
+      for (int q = 0; q < MAX_E / 32; ++q) {
+        const int e = lane + 32 * q;
+        if (e < E) acc[q] += expf(nan_to_ninf(__ldg(Lj + e)) - mj) * ij;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < MAX_E / 32; ++q) {
+      const int e = lane + 32 * q;
+      if (e < E) pw[warp][e] = acc[q];
+    }
   }
   __syncthreads();
-  // in-chunk ranks: token `local` handled by thread `local` (warp = 32 tokens in order)
-  const int local = threadIdx.x;
-  const uint64_t t = t0 + local;
+  // in-chunk ranks: thread = token, warp = 32 consecutive tokens in order
+  int ech[2] = {valid ? i1 : -1, (valid && k == 2) ? i2 : -1};
   int r_in[2] = {0, 0};
   for (int i = 0; i < k; ++i) {
-    const int e = ech[i][local];
+    const int e = ech[i];
     const unsigned peers = __match_any_sync(0xffffffffu, e);
     const unsigned lt = (1u << lane) - 1u;
     r_in[i] = __popc(peers & lt);
     if (e >= 0 && (peers & lt) == 0) hist[i][warp][e] = __popc(peers);
   }
   __syncthreads();
-  // per-warp exclusive offsets and chunk totals, one thread per (i, e)
   for (int x = threadIdx.x; x < k * E; x += RT_THREADS) {
     const int i = x / E, e = x % E;
     int run = 0;
@@ -155,16 +153,13 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
     chunk_cnt[((uint64_t)i * E + e) * nchunks + chunk] = run;
   }
   for (int e = threadIdx.x; e < E; e += RT_THREADS) {
-    float s = 0.f;
-    for (int w = 0; w < 8; ++w) s += pw[w][e];
-    psum_part[chunk * E + e] = s;
+    float sp = 0.f;
+    for (int w = 0; w < 8; ++w) sp += pw[w][e];
+    psum_part[chunk * E + e] = sp;
   }
   __syncthreads();
-  if (t < T) {
-    for (int i = 0; i < k; ++i) {
-      const int e = ech[i][local];
-      rank_local[t * k + i] = hist[i][warp][e] + r_in[i];
-    }
+  if (valid) {
+    for (int i = 0; i < k; ++i) rank_local[t * k + i] = hist[i][warp][ech[i]] + r_in[i];
   }
 }
 
@@ -463,78 +458,101 @@ __global__ void gather_dx_kernel(uint64_t T_, int d, int k, const T* __restrict_
   }
 }
 
-// Routing backward (DESIGN.md Appendix A §10), one warp per token.
+// Routing backward (DESIGN.md Appendix A §9), thread per token: recompute the
+// softmax from the stored logits, add the aux-loss term and the gate term, and
+// write the dlogits row (fp32 and/or the bf16 GEMM operand, pad columns zero).
 template <typename LP>
-__global__ void route_bwd_kernel(uint64_t T_, int E, int k, const float* __restrict__ logits,
-                                 const int32_t* __restrict__ expert, const float* __restrict__ gate,
-                                 const uint8_t* __restrict__ keep, const int32_t* __restrict__ count1,
-                                 const float* __restrict__ dgate, float d_aux,
-                                 float* __restrict__ dl_f32, LP* __restrict__ dl_lp, int ld,
-                                 float* __restrict__ dbg) {
+__global__ void __launch_bounds__(256) route_bwd_kernel(
+    uint64_t T_, int E, int k, const float* __restrict__ logits,
+    const int32_t* __restrict__ expert, const float* __restrict__ gate,
+    const uint8_t* __restrict__ keep, const int32_t* __restrict__ count1,
+    const float* __restrict__ dgate, float d_aux, float* __restrict__ dl_f32,
+    LP* __restrict__ dl_lp, int ld, float* __restrict__ dbg) {
+  __shared__ float a_s[MAX_E];
   __shared__ float dbg_s[MAX_E];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) dbg_s[e] = 0.f;
+  const float invT = 1.0f / (float)T_;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    a_s[e] = (float)E * (float)count1[e] * invT * invT;
+    dbg_s[e] = 0.f;
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t < T_) {
-    const float* L = logits + t * E;
-    float lv[MAX_E / 32], p[MAX_E / 32];
-    float m = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < MAX_E / 32; ++j) {
-      const int e = lane + 32 * j;
-      lv[j] = (e < E) ? nan_to_ninf(L[e]) : -INFINITY;
-      m = fmaxf(m, lv[j]);
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = t < T_;
+  const float* L = logits + (valid ? t : 0) * E;
+  float m = -INFINITY, z = 0.f, pnum = 0.f;
+  if (valid) {
+    for (int e = 0; e < E; ++e) m = fmaxf(m, nan_to_ninf(__ldg(L + e)));
+    for (int e = 0; e < E; ++e) {
+      const float ex = expf(nan_to_ninf(__ldg(L + e)) - m);
+      z += ex;
+      pnum = fmaf(ex, a_s[e], pnum);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    float z = 0.f;
-#pragma unroll
-    for (int j = 0; j < MAX_E / 32; ++j) {
-      const int e = lane + 32 * j;
-      p[j] = (e < E) ? expf(lv[j] - m) : 0.f;
-      z += p[j];
-    }
-    z = warp_sum(z);
-    const float invT = 1.0f / (float)T_;
-    float pa = 0.f;
-#pragma unroll
-    for (int j = 0; j < MAX_E / 32; ++j) {
-      const int e = lane + 32 * j;
-      p[j] /= z;
-      if (e < E) pa += p[j] * ((float)E * (float)count1[e] * invT * invT);
-    }
-    pa = warp_sum(pa);
-    // gate part
-    int e1 = expert[t * k], e2 = k == 2 ? expert[t * k + 1] : -1;
-    float dg1 = keep[t * k] ? dgate[t * k] : 0.f;
-    float v2 = 0.f;  // k=2: (dg1-dg2) g1 g2
-    float p1 = 0.f;
+  }
+  const float inv = valid ? 1.0f / z : 0.f;
+  const float pa = pnum * inv;
+  int e1 = -1, e2 = -1;
+  float gterm = 0.f, p1 = 0.f;
+  if (valid) {
+    e1 = expert[t * k];
+    const float dg1 = keep[t * k] ? dgate[t * k] : 0.f;
     if (k == 2) {
+      e2 = expert[t * k + 1];
       const float dg2 = keep[t * k + 1] ? dgate[t * k + 1] : 0.f;
-      v2 = (dg1 - dg2) * gate[t * k] * gate[t * k + 1];
+      gterm = (dg1 - dg2) * gate[t * k] * gate[t * k + 1];  // +/- on e1/e2
     } else {
+      gterm = dg1;
       p1 = gate[t];  // = p[e1]
     }
+  }
+  for (int e0 = 0; e0 < E; e0 += 8) {
+    float dl[8];
 #pragma unroll
-    for (int j = 0; j < MAX_E / 32; ++j) {
-      const int e = lane + 32 * j;
-      if (e >= E) continue;
-      const float a_e = (float)E * (float)count1[e] * invT * invT;
-      float dl = d_aux * p[j] * (a_e - pa);
-      if (k == 1) {
-        dl += dg1 * p1 * ((e == e1 ? 1.f : 0.f) - p[j]);
-      } else {
-        if (e == e1) dl += v2;
-        if (e == e2) dl -= v2;
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u;
+      float v = 0.f;
+      if (valid && e < E) {
+        const float pe = expf(nan_to_ninf(__ldg(L + e)) - m) * inv;
+        v = d_aux * pe * (a_s[e] - pa);
+        if (k == 1) v += gterm * p1 * ((e == e1 ? 1.f : 0.f) - pe);
+        else v += (e == e1 ? gterm : 0.f) - (e == e2 ? gterm : 0.f);
       }
-      if (dl_f32) dl_f32[t * E + e] = dl;
-      if (dl_lp) dl_lp[t * ld + e] = (LP)dl;
-      if (dbg) atomicAdd(&dbg_s[e], dl);
+      dl[u] = v;
     }
-    if (dl_lp) {
-      for (int e = E + lane; e < ld; e += 32) dl_lp[t * ld + e] = (LP)0.f;
+    if (valid) {
+      if (dl_f32) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e0 + u < E) dl_f32[t * E + e0 + u] = dl[u];
+      }
+      if (dl_lp) {
+        if (sizeof(LP) == 2 && (ld % 8) == 0 && e0 + 8 <= ld) {
+          uint4 o;
+          o.x = pack_bf16x2(dl[0], dl[1]);
+          o.y = pack_bf16x2(dl[2], dl[3]);
+          o.z = pack_bf16x2(dl[4], dl[5]);
+          o.w = pack_bf16x2(dl[6], dl[7]);
+          *reinterpret_cast<uint4*>(dl_lp + t * ld + e0) = o;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (e0 + u < ld) dl_lp[t * ld + e0 + u] = (LP)dl[u];
+        }
+      }
     }
+    if (dbg) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        float v = dl[u];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && e0 + u < E) atomicAdd(&dbg_s[e0 + u], v);
+      }
+    }
+  }
+  if (valid && dl_lp) {
+    const int from = ((E + 7) / 8) * 8;
+    for (int e = from; e < ld; ++e) dl_lp[t * ld + e] = (LP)0.f;
   }
   __syncthreads();
   if (dbg)
@@ -556,6 +574,42 @@ __global__ void colsum_kernel(const int32_t* __restrict__ gm, const int32_t* __r
   float s = 0.f;
   for (int r = r0; r < r1; ++r, base += N) s += (float)*base;
   atomicAdd(out + (uint64_t)gb[g] * N + n, s);
+}
+
+// bf16, 8 columns per thread (16-byte loads), 64 rows per block, 4 rows in flight
+__global__ void colsum_bf16x8_kernel(const int32_t* __restrict__ gm, const int32_t* __restrict__ ga,
+                                     const int32_t* __restrict__ gb, int N,
+                                     const __nv_bfloat16* __restrict__ X, float* __restrict__ out) {
+  const int g = blockIdx.x;
+  const int rows = gm[g];
+  const int r0 = blockIdx.y * 64;
+  if (r0 >= rows) return;
+  const int n = (blockIdx.z * blockDim.x + threadIdx.x) * 8;
+  if (n >= N) return;
+  const int r1 = min(rows, r0 + 64);
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const __nv_bfloat16* base = X + ((uint64_t)ga[g] + r0) * N + n;
+  int r = r0;
+  for (; r + 4 <= r1; r += 4, base += 4 * (uint64_t)N) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)u * N));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v[u]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
+    }
+  }
+  for (; r < r1; ++r, base += N) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(base));
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
+  }
+  float* o = out + (uint64_t)gb[g] * N + n;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) atomicAdd(o + q, acc[q]);
 }
 
 __global__ void build_groups_kernel(uint32_t P, uint32_t El, uint64_t Cs, const int32_t* cnt,
@@ -661,7 +715,7 @@ void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, con
                     const float* dgate, float d_aux, float* dlogits_f32, void* dlogits_lp,
                     moe_dtype_t lp_dtype, uint32_t ld, float* dbg, cudaStream_t st) {
   if (!T) return;
-  const unsigned blocks = (unsigned)ceil_div(T, 8);
+  const unsigned blocks = (unsigned)ceil_div(T, 256);
   if (dlogits_lp && lp_dtype == MOE_DTYPE_BF16)
     route_bwd_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
         T, (int)E, (int)k, logits, expert, gate, keep, count1, dgate, d_aux, dlogits_f32,
@@ -678,12 +732,17 @@ void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const i
                   uint32_t num_b, uint32_t N, moe_dtype_t dt, const void* X, float* out,
                   cudaStream_t st, uint64_t max_rows) {
   MOE_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (uint64_t)num_b * N, st));
-  dim3 grid(groups, (unsigned)ceil_div(max_rows, 128), (unsigned)ceil_div(N, 256));
-  if (dt == MOE_DTYPE_BF16)
-    colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(gm, ga, gb, (int)N,
-                                                       (const __nv_bfloat16*)X, out);
-  else
-    colsum_kernel<float><<<grid, 256, 0, st>>>(gm, ga, gb, (int)N, (const float*)X, out);
+  if (dt == MOE_DTYPE_BF16 && N % 8 == 0) {
+    dim3 grid(groups, (unsigned)ceil_div(max_rows, 64), (unsigned)ceil_div(N / 8, 128));
+    colsum_bf16x8_kernel<<<grid, 128, 0, st>>>(gm, ga, gb, (int)N, (const __nv_bfloat16*)X, out);
+  } else {
+    dim3 grid(groups, (unsigned)ceil_div(max_rows, 128), (unsigned)ceil_div(N, 256));
+    if (dt == MOE_DTYPE_BF16)
+      colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(gm, ga, gb, (int)N,
+                                                         (const __nv_bfloat16*)X, out);
+    else
+      colsum_kernel<float><<<grid, 256, 0, st>>>(gm, ga, gb, (int)N, (const float*)X, out);
+  }
   MOE_LAUNCH_CHECK("colsum_kernel");
   count_launch();
 }
