@@ -283,7 +283,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     return n;
   };
 
+  // Last block of a ragged group with <= 128 rows left: run it as an M = 128
+  // pair tile (each CTA 64 rows; TMEM lanes 0-63 hold output columns [0, BN/2),
+  // lanes 64-127 columns [BN/2, BN) — the 2-SM M=128 accumulator layout), which
+  // halves the padding waste of 256-row tiles.
+  auto is_tail = [&](int g, int mb) -> bool {
+    if (CG != 2 || KIND != 0) return false;
+    const int rem = args.gm[g] - mb * TM;
+    return rem > 0 && rem <= BM;
+  };
   constexpr uint32_t IDESC = umma_idesc_bf16(TM, BN, A_MN, B_MN);
+  constexpr uint32_t IDESC_T = umma_idesc_bf16(CG == 2 ? 128 : TM, BN, A_MN, B_MN);
   constexpr int BH = BN / CG;  // B columns held by this CTA
 
   if (warp == 0) {
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (crank == 0) mbar_arrive_expect_tx(&full[s], C_::STAGE_BYTES * CG);
         };
         if (KIND == 0) {
-          const int arow = args.ga[g] + mb * TM + (int)crank * BM;
+          const int arow = args.ga[g] + mb * TM + (int)crank * (is_tail(g, mb) ? 64 : BM);
           const int brow = args.gb[g] * (B_MN ? args.K : args.N);
           const int bcol = nb * BN + (int)crank * BH;
           const int nkb = args.K / BK;
@@ -354,6 +364,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         int g, mb, nb;
         decode(w, g, mb, nb);
         const int nkb = num_kblocks(g);
+        const uint32_t idesc = is_tail(g, mb) ? IDESC_T : IDESC;
         const uint32_t acc = tcount & 1;
         mbar_wait(&tempty[acc], ((tcount >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -370,8 +381,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                                      : umma_desc_sw128(aBase + kk * 32, 16, 1024);
             const uint64_t db = B_MN ? umma_desc_sw128(bBase + kk * 2048, 8192, 1024)
                                      : umma_desc_sw128(bBase + kk * 32, 16, 1024);
-            if (CG == 2) tc_mma_bf16_2sm(d_tmem, da, db, IDESC, (kb | kk) != 0 ? 1u : 0u);
-            else tc_mma_bf16(d_tmem, da, db, IDESC, (kb | kk) != 0 ? 1u : 0u);
+            if (CG == 2) tc_mma_bf16_2sm(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+            else tc_mma_bf16(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           if (CG == 2) tc_commit_2sm_mc(&empty[s], 0x3);
           else tc_commit(&empty[s]);
@@ -386,7 +397,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;           // TMEM lane quarter (hardware: warp % 4)
     const int half = ew >> 2;         // column half of the tile
     constexpr int HALF = BN / 2;
-    constexpr int NCH = (HALF + CW - 1) / CW;
     uint8_t* stg = smem + C_::EPI_OFF + ew * C_::WARP_EPI_BYTES;  // out [, out2] [, aux0, aux1]
     uint8_t* stg2 = stg + STG;
     uint8_t* auxb = stg + C_::NOUT * STG;
@@ -397,7 +407,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int w = unit; w < total_work; w += nunits, ++tcount) {
       int g, mb, nb;
       decode(w, g, mb, nb);
-      const int row0 = mb * TM + (int)crank * BM + q * 32;  // first tile row of this warp
+      const bool tail = is_tail(g, mb);
+      // first tile row / column of this warp, TMEM column offset, chunk count
+      const int row0 = tail ? mb * TM + (int)crank * 64 + (q & 1) * 32
+                            : mb * TM + (int)crank * BM + q * 32;
+      const int tcol = tail ? half * (BN / 4) : half * HALF;
+      const int nch = (tail ? BN / 4 : HALF) / CW;
       int nvalid, bidx;
       long long orow0;
       if (KIND == 0) {
@@ -433,7 +448,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         return sidx;
       };
-      const int col_base = nb * BN + half * HALF;
+      const int col_base = nb * BN + (tail ? (q >> 1) * (BN / 2) : 0) + tcol;
       if (EPI == MOE_EPI_DGELU && lane == 0 && col_base < args.N) {
         mbar_arrive_expect_tx(&ab[0], STG);
         tma_load_2d(auxb, &tmAux, &ab[0], col_base, (int)orow0);
@@ -448,9 +463,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t acc = tcount & 1;
       mbar_wait(&tfull[acc], (tcount >> 1) & 1);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * HALF;
+      const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + tcol;
 #pragma unroll 1
-      for (int c = 0; c < NCH; ++c) {
+      for (int c = 0; c < nch; ++c) {
         __syncwarp();
         float f[CW];
         {
@@ -462,7 +477,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int i = 0; i < CW; ++i) f[i] = has_k ? __uint_as_float(v[i]) : 0.0f;
         }
         const int n0 = col_base + c * CW;
-        if (EPI == MOE_EPI_DGELU && lane == 0 && c + 1 < NCH && n0 + CW < args.N) {
+        if (EPI == MOE_EPI_DGELU && lane == 0 && c + 1 < nch && n0 + CW < args.N) {
           mbar_arrive_expect_tx(&ab[(c + 1) & 1], STG);
           tma_load_2d(auxb + ((c + 1) & 1) * STG, &tmAux, &ab[(c + 1) & 1], n0 + CW, (int)orow0);
         }
