@@ -45,15 +45,19 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_HEAVY = (EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU) ? 1 : 0;
-  static constexpr int STAGES =
-      (CG == 2) ? (EPI_HEAVY ? 5 : 6)
-                : ((BN == 256) ? (EPI_HEAVY ? 3 : 4) : (BN == 128 ? 6 : 8));
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int CW = CF32 ? 16 : 32;  // epilogue chunk width (columns): 64B per row
   static constexpr int NOUT = (EPI == MOE_EPI_GELU) ? 2 : 1;
   static constexpr int NAUX = (EPI == MOE_EPI_DGELU) ? 2 : 0;
-  static constexpr int WARP_EPI_BYTES = (NOUT + NAUX) * STG;
+  // output staging buffers per warp: double-buffered (the TMA store of chunk c
+  // drains while chunk c+1 is computed) where the epilogue is the long pole
+  static constexpr int NBUF = (EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU || CF32) ? 2 : 1;
+  static constexpr int WARP_EPI_BYTES = (NBUF * NOUT + NAUX) * STG;
+  // as many operand stages as fit next to the epilogue buffers (<= 8)
+  static constexpr int FIT =
+      (232448 - 6 * 1024 - EPI_WARPS * WARP_EPI_BYTES - (MAX_GROUPS + 1) * 4) / STAGE_BYTES;
+  static constexpr int STAGES = FIT > 8 ? 8 : FIT;
+  static_assert(STAGES >= 3, "pipeline depth");
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = EPI_OFF + EPI_WARPS * WARP_EPI_BYTES;
   static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * EPI_WARPS) * 8;
@@ -397,9 +401,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int q = warp & 3;           // TMEM lane quarter (hardware: warp % 4)
     const int half = ew >> 2;         // column half of the tile
     constexpr int HALF = BN / 2;
-    uint8_t* stg = smem + C_::EPI_OFF + ew * C_::WARP_EPI_BYTES;  // out [, out2] [, aux0, aux1]
-    uint8_t* stg2 = stg + STG;
-    uint8_t* auxb = stg + C_::NOUT * STG;
+    // out[NBUF] [, out2[NBUF]] [, aux[2]]
+    uint8_t* const stg_base = smem + C_::EPI_OFF + ew * C_::WARP_EPI_BYTES;
+    uint8_t* const auxb = stg_base + C_::NBUF * C_::NOUT * STG;
+    uint32_t nst = 0;  // bulk store groups committed by this warp (selects the buffer)
     uint64_t* ab = abar + 2 * ew;
     uint32_t aph[2] = {0, 0};
     uint32_t tcount = 0;
@@ -487,6 +492,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           aph[c & 1] ^= 1;
         }
         if (nvalid == 0) continue;
+        uint8_t* const stg = stg_base + (C_::NBUF == 2 ? (nst & 1) : 0) * STG;
+        uint8_t* const stg2 = stg_base + (C_::NBUF + (C_::NBUF == 2 ? (nst & 1) : 0)) * STG;
         const int ncols = min(CW, args.N - n0);
         const bool full_tile = nvalid == 32 && ncols == CW;
         const bool row_ok = lane < nvalid;
@@ -506,8 +513,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (args.bias != nullptr && EPI != MOE_EPI_DGELU && EPI != MOE_EPI_GATHER_ADD) {
           const float* bp = args.bias + (long long)bidx * args.N + n0;
+          if (ncols == CW && (args.N & 3) == 0 && (reinterpret_cast<uintptr_t>(args.bias) & 15) == 0) {
 #pragma unroll
-          for (int i = 0; i < CW; ++i) f[i] += (i < ncols) ? bp[i] : 0.0f;
+            for (int i = 0; i < CW; i += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bp + i));
+              f[i] += b4.x;
+              f[i + 1] += b4.y;
+              f[i + 2] += b4.z;
+              f[i + 3] += b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < CW; ++i) f[i] += (i < ncols) ? bp[i] : 0.0f;
+          }
         }
         float f2[CW];
         if (EPI == MOE_EPI_GELU) {
@@ -548,7 +566,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int s1 = __shfl_sync(0xffffffffu, sl, max(nvalid - 1, 0));
           const int off0 = __shfl_sync(0xffffffffu, rexcl, s0);
           if (full_tile && s0 == s1) {
-            if (lane == 0) bulk_wait_read0();
+            if (lane == 0) {
+              if (C_::NBUF == 2) bulk_wait_read1();
+              else bulk_wait_read0();
+            }
             __syncwarp();
             stage_row<CF32>(stg, lane, f);
             fence_proxy_async_smem();
@@ -557,6 +578,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               tma_store_2d(&ro.maps[s0], stg, n0, (int)(rexp * ro.Cs + row0 - off0));
               bulk_commit();
             }
+            ++nst;
           } else if (row_ok) {
             uint8_t* dst = ro.peers[sl] + ro.home_off;
             store_row_direct<CF32>(dst, (rexp * ro.Cs + row0 + lane - offl) * args.ldc + n0,
@@ -566,7 +588,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         const bool want_colsum = EPI == MOE_EPI_DGELU && args.colsum != nullptr;
         if (full_tile || want_colsum) {
-          if (lane == 0) bulk_wait_read0();  // previous store out of this buffer is done
+          if (lane == 0) {  // the store that last used this buffer has read it
+            if (C_::NBUF == 2) bulk_wait_read1();
+            else bulk_wait_read0();
+          }
           __syncwarp();
           if (!row_ok) {
 #pragma unroll
@@ -581,6 +606,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (EPI == MOE_EPI_GELU) tma_store_2d(&tmC2, stg2, n0, (int)orow0);
             bulk_commit();
           }
+          if (full_tile) ++nst;
         }
         if (!full_tile && row_ok) {
           const long long off = (orow0 + lane) * args.ldc + n0;
@@ -602,7 +628,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster(mapa_shared(tempty0 + acc * 8, 0));
+        if (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(tempty0 + acc * 8, 0));
         else mbar_arrive(&tempty[acc]);
       }
     }
