@@ -277,7 +277,7 @@ moe_status_t moe_route(uint64_t tokens, uint32_t experts, uint32_t top_k, uint64
     };
     ws.chunk_cnt = (int32_t*)al(2 * ws.nchunks * experts * 4);
     ws.chunk_off = (int32_t*)al(2 * ws.nchunks * experts * 4);
-    ws.psum_part = (float*)al(ws.nchunks * experts * 4);
+    ws.psum_part = (float*)al((ws.nchunks + 1) * experts * 4);
     ws.rank_local = (int32_t*)al(tokens * top_k * 4);
     moe::route_forward(tokens, experts, top_k, capacity, logits, *out, ws, S(stream));
     for (void* p : tmp) MOE_CUDA(cudaFreeAsync(p, S(stream)));

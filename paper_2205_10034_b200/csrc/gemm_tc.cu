@@ -48,7 +48,8 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int CW = CF32 ? 16 : 32;  // epilogue chunk width (columns): 64B per row
   static constexpr int NOUT = (EPI == MOE_EPI_GELU) ? 2 : 1;
-  static constexpr int NAUX = (EPI == MOE_EPI_DGELU) ? 2 : 0;
+  // DGELU: aux tile (TMA, double-buffered); GATHER_ADD: 2 gathered sources x 2 buffers
+  static constexpr int NAUX = (EPI == MOE_EPI_DGELU) ? 2 : (EPI == MOE_EPI_GATHER_ADD ? 4 : 0);
   // output staging buffers per warp: double-buffered (the TMA store of chunk c
   // drains while chunk c+1 is computed) where the epilogue is the long pole
   static constexpr int NBUF = (EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU || CF32) ? 2 : 1;
@@ -464,6 +465,24 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < 2; ++i)
           if (i < args.gk) gidx[i] = args.gidx[(orow0 + lane) * args.gk + i];
       }
+      // GATHER_ADD: this lane's gathered 64-byte row pieces of chunk cc go to
+      // aux buffer [i][cc & 1] (swizzled like the staging tiles), one chunk ahead
+      auto gather_prefetch = [&](int cc) {
+        const int nn = col_base + cc * CW;
+        if (nn + CW <= args.N) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            if (gidx[i] < 0) continue;
+            const __nv_bfloat16* src =
+                reinterpret_cast<const __nv_bfloat16*>(args.gsrc) + (long long)gidx[i] * args.N + nn;
+            const uint32_t dst = smem_u32(auxb + (i * 2 + (cc & 1)) * STG);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cp_async16(dst + sw64(lane, j), src + j * 8);
+          }
+        }
+        cp_async_commit();
+      };
+      if (EPI == MOE_EPI_GATHER_ADD) gather_prefetch(0);
       const bool has_k = num_kblocks(g) > 0;
       const uint32_t acc = tcount & 1;
       mbar_wait(&tfull[acc], (tcount >> 1) & 1);
@@ -485,6 +504,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (EPI == MOE_EPI_DGELU && lane == 0 && c + 1 < nch && n0 + CW < args.N) {
           mbar_arrive_expect_tx(&ab[(c + 1) & 1], STG);
           tma_load_2d(auxb + ((c + 1) & 1) * STG, &tmAux, &ab[(c + 1) & 1], n0 + CW, (int)orow0);
+        }
+        if (EPI == MOE_EPI_GATHER_ADD) {
+          if (c + 1 < nch) gather_prefetch(c + 1);
+          else cp_async_commit();  // keep one group per chunk
         }
         if (n0 >= args.N) continue;
         if (EPI == MOE_EPI_DGELU) {
@@ -517,10 +540,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int i = 0; i < CW; i += 4) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(bp + i));
-              f[i] += b4.x;
-              f[i + 1] += b4.y;
-              f[i + 2] += b4.z;
-              f[i + 3] += b4.w;
+              const float2 lo = __fadd2_rn(make_float2(f[i], f[i + 1]), make_float2(b4.x, b4.y));
+              const float2 hi = __fadd2_rn(make_float2(f[i + 2], f[i + 3]), make_float2(b4.z, b4.w));
+              f[i] = lo.x;
+              f[i + 1] = lo.y;
+              f[i + 2] = hi.x;
+              f[i + 3] = hi.y;
             }
           } else {
 #pragma unroll
@@ -530,30 +555,55 @@ __global__ void __launch_bounds__(THREADS, 1)
         float f2[CW];
         if (EPI == MOE_EPI_GELU) {
 #pragma unroll
-          for (int i = 0; i < CW; ++i) gelu_and_grad_fast(f[i], f[i], f2[i]);
+          for (int i = 0; i < CW; i += 2) {
+            float2 a2, g2;
+            gelu_and_grad_x2(make_float2(f[i], f[i + 1]), a2, g2);
+            f[i] = a2.x;
+            f[i + 1] = a2.y;
+            f2[i] = g2.x;
+            f2[i + 1] = g2.y;
+          }
         }
         if (EPI == MOE_EPI_DGELU) {
           const uint8_t* ax = auxb + (c & 1) * STG;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const uint4 hv = *reinterpret_cast<const uint4*>(ax + sw64(lane, j));
-            const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&hv);
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-            for (int i = 0; i < 8; ++i) f[j * 8 + i] *= bf2f(h8[i]);
+            for (int i = 0; i < 4; ++i) {
+              const float2 m = __fmul2_rn(make_float2(f[j * 8 + 2 * i], f[j * 8 + 2 * i + 1]),
+                                          bf16x2_to_float2(hw[i]));
+              f[j * 8 + 2 * i] = m.x;
+              f[j * 8 + 2 * i + 1] = m.y;
+            }
           }
         }
         if (EPI == MOE_EPI_GATHER_ADD) {
+          cp_async_wait<1>();  // this chunk's rows (the next chunk's may be in flight)
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            if (i >= args.gk || gidx[i] < 0) continue;
-            const __nv_bfloat16* src =
-                reinterpret_cast<const __nv_bfloat16*>(args.gsrc) + (long long)gidx[i] * args.N + n0;
+            if (gidx[i] < 0) continue;
+            if (ncols == CW) {
+              const uint8_t* gb = auxb + (i * 2 + (c & 1)) * STG;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const uint4 hv = *reinterpret_cast<const uint4*>(src + j * 8);
-              const __nv_bfloat16* h8 = reinterpret_cast<const __nv_bfloat16*>(&hv);
+              for (int j = 0; j < 4; ++j) {
+                const uint4 hv = *reinterpret_cast<const uint4*>(gb + sw64(lane, j));
+                const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
-              for (int u = 0; u < 8; ++u) f[j * 8 + u] += bf2f(h8[u]);
+                for (int u = 0; u < 4; ++u) {
+                  const float2 a2 = __fadd2_rn(make_float2(f[j * 8 + 2 * u], f[j * 8 + 2 * u + 1]),
+                                               bf16x2_to_float2(hw[u]));
+                  f[j * 8 + 2 * u] = a2.x;
+                  f[j * 8 + 2 * u + 1] = a2.y;
+                }
+              }
+            } else {
+              const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(args.gsrc) +
+                                         (long long)gidx[i] * args.N + n0;
+#pragma unroll
+              for (int u = 0; u < CW; ++u)
+                if (u < ncols) f[u] += bf2f(src[u]);
             }
           }
         }
@@ -615,14 +665,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (want_colsum && !CF32) {
           // column sums of the stored (bf16-rounded) values, rows >= nvalid are zero
-          if (lane < ncols) {
-            float s = 0.f;
-            const uint32_t j = lane >> 3, e = lane & 7;
-#pragma unroll 8
-            for (int r = 0; r < 32; ++r)
-              s += bf2f(*reinterpret_cast<const __nv_bfloat16*>(stg + sw64(r, j) + e * 2));
-            atomicAdd(args.colsum + (long long)bidx * args.N + n0 + lane, s);
+          // lane = (row parity, column pair): 16 x 4-byte reads per lane,
+          // even/odd rows sit in opposite bank halves
+          const uint32_t cp = lane & 15, rp = lane >> 4;
+          float2 s = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(
+                stg + sw64(2 * r + rp, cp >> 2) + (cp & 3) * 4);
+            s = __fadd2_rn(s, bf16x2_to_float2(w));
           }
+          s.x += __shfl_xor_sync(0xffffffffu, s.x, 16);
+          s.y += __shfl_xor_sync(0xffffffffu, s.y, 16);
+          float* cs = args.colsum + (long long)bidx * args.N + n0 + 2 * cp;
+          if (rp == 0 && 2 * (int)cp < ncols) atomicAdd(cs, s.x);
+          if (rp == 0 && 2 * (int)cp + 1 < ncols) atomicAdd(cs + 1, s.y);
         }
       }
       tc_fence_before();

@@ -41,7 +41,7 @@ inline void grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st,
 struct RouteWorkspace {
   int32_t* chunk_cnt = nullptr;  // [2][nchunks][E]
   int32_t* chunk_off = nullptr;  // [2][nchunks][E]
-  float* psum_part = nullptr;    // [nchunks][E]
+  float* psum_part = nullptr;    // [E][nchunks] partial softmax mass, then [E] totals
   int32_t* rank_local = nullptr; // [T][k]
   uint64_t nchunks = 0;
 };

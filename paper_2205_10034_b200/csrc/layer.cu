@@ -106,7 +106,7 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   rws.nchunks = route_chunks(T);
   rws.chunk_cnt = dalloc<int32_t>(owned, 2 * rws.nchunks * E);
   rws.chunk_off = dalloc<int32_t>(owned, 2 * rws.nchunks * E);
-  rws.psum_part = dalloc<float>(owned, rws.nchunks * E);
+  rws.psum_part = dalloc<float>(owned, (rws.nchunks + 1) * E);
   rws.rank_local = dalloc<int32_t>(owned, T * k);
   // token buffers
   const uint64_t slot_bytes = (uint64_t)E * Cs * dm * esz;

@@ -25,6 +25,9 @@ namespace {
 constexpr int CHUNK = 256;  // tokens per routing block (8 warps x 32)
 constexpr int RT_THREADS = 256;
 constexpr int MAX_E = 256;
+constexpr int SLAB = 64;        // experts per shared-memory slab of logits
+constexpr int TS = SLAB + 1;    // padded row stride (floats): row and column reads conflict-free
+constexpr int SLAB_SMEM = CHUNK * TS * 4;
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -33,62 +36,81 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 __device__ __forceinline__ float nan_to_ninf(float v) { return isnan(v) ? -INFINITY : v; }
 
+// Stage logits[t0, t0 + CHUNK) x [e0, e0 + ne) into tile[CHUNK][TS] (NaN read
+// as -inf, missing rows/columns -inf): each warp instruction reads 128
+// contiguous bytes of one row, so the thread-per-token passes below read
+// shared memory instead of issuing 32-row-wide scattered global loads.
+__device__ __forceinline__ void load_slab(const float* __restrict__ logits, uint64_t t0, uint64_t T,
+                                          int E, int e0, int ne, float* tile) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int r = warp; r < CHUNK; r += RT_THREADS / 32) {
+    const uint64_t t = t0 + r;
+    const float* L = logits + t * E + e0;
+#pragma unroll
+    for (int j = lane; j < SLAB; j += 32) {
+      float v = -INFINITY;
+      if (t < T && j < ne) v = nan_to_ninf(__ldg(L + j));
+      tile[r * TS + j] = v;
+    }
+  }
+}
+
 // Phase A: thread per token (the block is one 256-token chunk): top-k on the
 // fp32 logits, softmax, gates; per chunk: histograms (expert-major
 // [i][E][nchunks]), in-chunk ranks (warp match over 32 consecutive tokens +
 // per-warp histograms), and softmax column partial sums reduced in a fixed
-// order (deterministic aux loss).
+// order (deterministic aux loss), written expert-major [E][nchunks].
 __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
     uint64_t T, int E, int k, const float* __restrict__ logits, int32_t* __restrict__ expert,
     float* __restrict__ gate, int32_t* __restrict__ rank_local, int32_t* __restrict__ chunk_cnt,
     float* __restrict__ psum_part, uint64_t nchunks) {
+  extern __shared__ float tile[];  // [CHUNK][TS]
   __shared__ int hist[2][8][MAX_E];
   __shared__ float pw[8][MAX_E];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ float mrow[CHUNK], irow[CHUNK];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const uint64_t chunk = blockIdx.x;
-  const uint64_t t = chunk * CHUNK + threadIdx.x;
+  const uint64_t t0 = chunk * CHUNK;
+  const uint64_t t = t0 + tid;
   const bool valid = t < T;
+  const int nslab = (E + SLAB - 1) / SLAB;
 
-  for (int i = threadIdx.x; i < 2 * 8 * MAX_E; i += RT_THREADS) (&hist[0][0][0])[i] = 0;
+  for (int i = tid; i < 2 * 8 * MAX_E; i += RT_THREADS) (&hist[0][0][0])[i] = 0;
 
   // pass 1: top-1 / top-2 on logits (NaN read as -inf, ties to the lowest index)
-  const float4* L4 = reinterpret_cast<const float4*>(logits + t * E);
-  const float* L = logits + t * E;
   float v1 = -INFINITY, v2 = -INFINITY;
   int i1 = 0x7fffffff, i2 = 0x7fffffff;
-  auto consider = [&](float v, int e) {
-    v = nan_to_ninf(v);
-    if (v > v1 || (v == v1 && e < i1)) {
-      v2 = v1; i2 = i1; v1 = v; i1 = e;
-    } else if (v > v2 || (v == v2 && e < i2)) {
-      v2 = v; i2 = e;
-    }
-  };
-  const bool vec = (E % 4) == 0;
-  if (valid) {
-    if (vec) {
-      for (int q = 0; q < E / 4; ++q) {
-        const float4 f = __ldg(L4 + q);
-        consider(f.x, 4 * q);
-        consider(f.y, 4 * q + 1);
-        consider(f.z, 4 * q + 2);
-        consider(f.w, 4 * q + 3);
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int e0 = sl * SLAB, ne = min(SLAB, E - e0);
+    __syncthreads();
+    load_slab(logits, t0, T, E, e0, ne, tile);
+    __syncthreads();
+    if (valid) {
+      const float* row = tile + tid * TS;
+      for (int j = 0; j < ne; ++j) {
+        const float v = row[j];
+        const int e = e0 + j;
+        if (v > v1 || (v == v1 && e < i1)) {
+          v2 = v1; i2 = i1; v1 = v; i1 = e;
+        } else if (v > v2 || (v == v2 && e < i2)) {
+          v2 = v; i2 = e;
+        }
       }
-    } else {
-      for (int e = 0; e < E; ++e) consider(__ldg(L + e), e);
     }
   }
-  // pass 2: softmax denominator (max = v1)
+  // pass 2: softmax denominator (max = v1), experts in index order
   float z = 0.f;
-  if (valid) {
-    if (vec) {
-      for (int q = 0; q < E / 4; ++q) {
-        const float4 f = __ldg(L4 + q);
-        z += expf(nan_to_ninf(f.x) - v1) + expf(nan_to_ninf(f.y) - v1) +
-             expf(nan_to_ninf(f.z) - v1) + expf(nan_to_ninf(f.w) - v1);
-      }
-    } else {
-      for (int e = 0; e < E; ++e) z += expf(nan_to_ninf(__ldg(L + e)) - v1);
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int e0 = sl * SLAB, ne = min(SLAB, E - e0);
+    if (nslab > 1) {
+      __syncthreads();
+      load_slab(logits, t0, T, E, e0, ne, tile);
+      __syncthreads();
+    }
+    if (valid) {
+      const float* row = tile + tid * TS;
+      for (int j = 0; j < ne; ++j) z += expf(row[j] - v1);
     }
   }
   const float inv = valid ? 1.0f / z : 0.f;
@@ -105,30 +127,30 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
       gate[2 * t + 1] = p2 / sden;
     }
   }
-  // pass 3: softmax column sums over the warp's 32 tokens: lane l owns experts
-  // l, l+32, ...; token j's (max, 1/z) broadcast from lane j; rows read
-  // coalesced.  Then a fixed-order sum over the 8 warps (deterministic aux).
-  {
-    float acc[MAX_E / 32];
+  mrow[tid] = v1;
+  irow[tid] = inv;
+  // pass 3: softmax column sums over the warp's 32 tokens (lane = expert
+  // column), then a fixed-order sum over the 8 warps (deterministic aux)
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int e0 = sl * SLAB, ne = min(SLAB, E - e0);
+    __syncthreads();
+    if (nslab > 1) {
+      load_slab(logits, t0, T, E, e0, ne, tile);
+      __syncthreads();
+    }
+    float acc[SLAB / 32];
 #pragma unroll
-    for (int q = 0; q < MAX_E / 32; ++q) acc[q] = 0.f;
-    const uint64_t t0w = chunk * CHUNK + warp * 32;
+    for (int q = 0; q < SLAB / 32; ++q) acc[q] = 0.f;
     for (int j = 0; j < 32; ++j) {
-      const float mj = __shfl_sync(0xffffffffu, v1, j);
-      const float ij = __shfl_sync(0xffffffffu, inv, j);
-      if (t0w + j >= T) break;
-      const float* Lj = logits + (t0w + j) * E;
+      const int r = warp * 32 + j;
+      if (t0 + r >= T) break;
+      const float mj = mrow[r], ij = irow[r];
 #pragma unroll
-      for (int q = 0; q < MAX_E / 32; ++q) {
-        const int e = lane + 32 * q;
-        if (e < E) acc[q] += expf(nan_to_ninf(__ldg(Lj + e)) - mj) * ij;
-      }
+      for (int q = 0; q < SLAB / 32; ++q) acc[q] += expf(tile[r * TS + lane + 32 * q] - mj) * ij;
     }
 #pragma unroll
-    for (int q = 0; q < MAX_E / 32; ++q) {
-      const int e = lane + 32 * q;
-      if (e < E) pw[warp][e] = acc[q];
-    }
+    for (int q = 0; q < SLAB / 32; ++q)
+      if (lane + 32 * q < ne) pw[warp][e0 + lane + 32 * q] = acc[q];
   }
   __syncthreads();
   // in-chunk ranks: thread = token, warp = 32 consecutive tokens in order
@@ -142,7 +164,7 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
     if (e >= 0 && (peers & lt) == 0) hist[i][warp][e] = __popc(peers);
   }
   __syncthreads();
-  for (int x = threadIdx.x; x < k * E; x += RT_THREADS) {
+  for (int x = tid; x < k * E; x += RT_THREADS) {
     const int i = x / E, e = x % E;
     int run = 0;
     for (int w = 0; w < 8; ++w) {
@@ -152,10 +174,10 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
     }
     chunk_cnt[((uint64_t)i * E + e) * nchunks + chunk] = run;
   }
-  for (int e = threadIdx.x; e < E; e += RT_THREADS) {
+  for (int e = tid; e < E; e += RT_THREADS) {
     float sp = 0.f;
     for (int w = 0; w < 8; ++w) sp += pw[w][e];
-    psum_part[chunk * E + e] = sp;
+    psum_part[(uint64_t)e * nchunks + chunk] = sp;
   }
   __syncthreads();
   if (valid) {
@@ -163,80 +185,80 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
   }
 }
 
+// Exclusive scan of one expert's chunk counts by one warp: lane l owns the
+// contiguous chunk range [l*per, (l+1)*per); all loads of a pass are
+// independent.  Returns the total.
+__device__ __forceinline__ int warp_chunk_scan(const int32_t* __restrict__ cc,
+                                               int32_t* __restrict__ co, uint64_t nchunks,
+                                               int base) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t per = (nchunks + 31) / 32;
+  const uint64_t c0 = lane * per, c1 = min(nchunks, c0 + per);
+  int mine = 0;
+  for (uint64_t c = c0; c < c1; ++c) mine += cc[c];
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  int run = base + incl - mine;
+  for (uint64_t c = c0; c < c1; ++c) {
+    const int v = cc[c];
+    co[c] = run;
+    run += v;
+  }
+  return base + __shfl_sync(0xffffffffu, incl, 31);
+}
+
 // Phase B: per-expert exclusive scan over chunks (one warp per expert),
-// counts, kept, aux loss.  Single block.
-__global__ void __launch_bounds__(1024) route_scan_kernel(
+// counts, kept, per-expert softmax mass (fixed-order sum).
+__global__ void __launch_bounds__(256) route_scan_kernel(
     uint64_t T, int E, int k, uint64_t C, const int32_t* __restrict__ chunk_cnt,
     int32_t* __restrict__ chunk_off, const float* __restrict__ psum_part, uint64_t nchunks,
     int32_t* __restrict__ count1, int32_t* __restrict__ count2, int32_t* __restrict__ kept,
-    float* __restrict__ aux) {
-  __shared__ float auxe[MAX_E];
-  __shared__ int c1s[MAX_E];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int e = warp; e < E; e += nw) {
-    // top-1
-    const int32_t* cc = chunk_cnt + (uint64_t)e * nchunks;
-    int32_t* co = chunk_off + (uint64_t)e * nchunks;
-    int carry = 0;
-    float ps = 0.f;
-    for (uint64_t base = 0; base < nchunks; base += 32) {
-      const uint64_t c = base + lane;
-      const int v = c < nchunks ? cc[c] : 0;
-      int incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
-      }
-      if (c < nchunks) co[c] = carry + incl - v;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-      if (c < nchunks) ps += psum_part[c * E + e];
-    }
-    ps = warp_sum(ps);
-    const int c1 = carry;
-    int c2 = 0;
-    if (k == 2) {
-      const int32_t* cc2 = chunk_cnt + ((uint64_t)E + e) * nchunks;
-      int32_t* co2 = chunk_off + ((uint64_t)E + e) * nchunks;
-      int carry2 = c1;  // top-2 positions start after all (pre-drop) top-1 tokens
-      for (uint64_t base = 0; base < nchunks; base += 32) {
-        const uint64_t c = base + lane;
-        const int v = c < nchunks ? cc2[c] : 0;
-        int incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int u = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += u;
-        }
-        if (c < nchunks) co2[c] = carry2 + incl - v;
-        carry2 += __shfl_sync(0xffffffffu, incl, 31);
-      }
-      c2 = carry2 - c1;
-    }
-    if (lane == 0) {
-      count1[e] = c1;
-      count2[e] = c2;
-      const uint64_t tot = (uint64_t)c1 + (uint64_t)c2;
-      kept[e] = (int32_t)(tot < C ? tot : C);
-      auxe[e] = ps;
-      c1s[e] = c1;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0;
-    const double invT = T ? 1.0 / (double)T : 0.0;
-    for (int e = 0; e < E; ++e) a += ((double)auxe[e] * invT) * ((double)c1s[e] * invT);
-    aux[0] = (float)((double)E * a);
+    float* __restrict__ psum_e) {
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (e >= E) return;
+  const int c1 = warp_chunk_scan(chunk_cnt + (uint64_t)e * nchunks,
+                                 chunk_off + (uint64_t)e * nchunks, nchunks, 0);
+  int c2 = 0;
+  if (k == 2)  // top-2 positions start after all (pre-drop) top-1 tokens
+    c2 = warp_chunk_scan(chunk_cnt + ((uint64_t)E + e) * nchunks,
+                         chunk_off + ((uint64_t)E + e) * nchunks, nchunks, c1) - c1;
+  const uint64_t per = (nchunks + 31) / 32;
+  const uint64_t q0 = lane * per, q1 = min(nchunks, q0 + per);
+  float ps = 0.f;
+  for (uint64_t c = q0; c < q1; ++c) ps += psum_part[(uint64_t)e * nchunks + c];
+  ps = warp_sum(ps);
+  if (lane == 0) {
+    count1[e] = c1;
+    count2[e] = c2;
+    const uint64_t tot = (uint64_t)c1 + (uint64_t)c2;
+    kept[e] = (int32_t)(tot < C ? tot : C);
+    psum_e[e] = ps;
   }
 }
 
-// Phase C: positions and keep flags.
+// Phase C: positions and keep flags; block 0 / warp 0 also forms the aux loss
+// E * sum_e (psum_e / T) (count1_e / T) in a fixed order.
 __global__ void route_finalize_kernel(uint64_t T, int E, int k, uint64_t C, uint64_t nchunks,
                                       const int32_t* __restrict__ expert,
                                       const int32_t* __restrict__ rank_local,
                                       const int32_t* __restrict__ chunk_off,
-                                      int32_t* __restrict__ position, uint8_t* __restrict__ keep) {
+                                      int32_t* __restrict__ position, uint8_t* __restrict__ keep,
+                                      const float* __restrict__ psum_e,
+                                      const int32_t* __restrict__ count1, float* __restrict__ aux) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const double invT = T ? 1.0 / (double)T : 0.0;
+    double a = 0.0;
+    for (int e = threadIdx.x; e < E; e += 32)
+      a += ((double)psum_e[e] * invT) * ((double)count1[e] * invT);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (threadIdx.x == 0) aux[0] = (float)((double)E * a);
+  }
   const uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= T * k) return;
   const uint64_t t = x / k;
@@ -264,18 +286,22 @@ void route_forward(uint64_t T, uint32_t E, uint32_t k, uint64_t C, const float* 
     MOE_CUDA(cudaMemsetAsync(out.aux_loss, 0, sizeof(float), st));
     return;
   }
+  MOE_CUDA(cudaFuncSetAttribute(route_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                SLAB_SMEM));
   const uint64_t nch = route_chunks(T);
-  route_topk_kernel<<<(unsigned)nch, RT_THREADS, 0, st>>>(T, (int)E, (int)k, logits, out.expert,
-                                                          out.gate, ws.rank_local, ws.chunk_cnt,
-                                                          ws.psum_part, nch);
+  float* psum_e = ws.psum_part + nch * E;
+  route_topk_kernel<<<(unsigned)nch, RT_THREADS, SLAB_SMEM, st>>>(
+      T, (int)E, (int)k, logits, out.expert, out.gate, ws.rank_local, ws.chunk_cnt, ws.psum_part,
+      nch);
   MOE_LAUNCH_CHECK("route_topk_kernel");
-  route_scan_kernel<<<1, 1024, 0, st>>>(T, (int)E, (int)k, C, ws.chunk_cnt, ws.chunk_off,
-                                        ws.psum_part, nch, out.count1, out.count2, out.kept,
-                                        out.aux_loss);
+  route_scan_kernel<<<(E + 7) / 8, 256, 0, st>>>(T, (int)E, (int)k, C, ws.chunk_cnt, ws.chunk_off,
+                                                 ws.psum_part, nch, out.count1, out.count2,
+                                                 out.kept, psum_e);
   MOE_LAUNCH_CHECK("route_scan_kernel");
   const uint64_t n = T * k;
   route_finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-      T, (int)E, (int)k, C, nch, out.expert, ws.rank_local, ws.chunk_off, out.position, out.keep);
+      T, (int)E, (int)k, C, nch, out.expert, ws.rank_local, ws.chunk_off, out.position, out.keep,
+      psum_e, out.count1, out.aux_loss);
   MOE_LAUNCH_CHECK("route_finalize_kernel");
   count_launch(3);
 }
@@ -458,36 +484,50 @@ __global__ void gather_dx_kernel(uint64_t T_, int d, int k, const T* __restrict_
   }
 }
 
-// Routing backward (DESIGN.md Appendix A §9), thread per token: recompute the
-// softmax from the stored logits, add the aux-loss term and the gate term, and
-// write the dlogits row (fp32 and/or the bf16 GEMM operand, pad columns zero).
+// Routing backward (DESIGN.md Appendix A §9), thread per token on a staged
+// 256-token slab of logits: recompute the softmax, add the aux-loss term and
+// the gate term, put the dlogits row back into the slab, then write the slab
+// out row-coalesced (fp32 and/or the bf16 GEMM operand, pad columns zero) and
+// reduce its columns into the gate-bias gradient.
 template <typename LP>
-__global__ void __launch_bounds__(256) route_bwd_kernel(
+__global__ void __launch_bounds__(RT_THREADS) route_bwd_kernel(
     uint64_t T_, int E, int k, const float* __restrict__ logits,
     const int32_t* __restrict__ expert, const float* __restrict__ gate,
     const uint8_t* __restrict__ keep, const int32_t* __restrict__ count1,
     const float* __restrict__ dgate, float d_aux, float* __restrict__ dl_f32,
     LP* __restrict__ dl_lp, int ld, float* __restrict__ dbg) {
+  extern __shared__ float tile[];  // [CHUNK][TS]
   __shared__ float a_s[MAX_E];
-  __shared__ float dbg_s[MAX_E];
+  __shared__ float cs[8][SLAB];
   const float invT = 1.0f / (float)T_;
-  for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    a_s[e] = (float)E * (float)count1[e] * invT * invT;
-    dbg_s[e] = 0.f;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  for (int e = tid; e < E; e += blockDim.x) a_s[e] = (float)E * (float)count1[e] * invT * invT;
+  const uint64_t t0 = (uint64_t)blockIdx.x * CHUNK;
+  const uint64_t t = t0 + tid;
   const bool valid = t < T_;
-  const float* L = logits + (valid ? t : 0) * E;
+  const int nslab = (E + SLAB - 1) / SLAB;
   float m = -INFINITY, z = 0.f, pnum = 0.f;
-  if (valid) {
-    for (int e = 0; e < E; ++e) m = fmaxf(m, nan_to_ninf(__ldg(L + e)));
-    for (int e = 0; e < E; ++e) {
-      const float ex = expf(nan_to_ninf(__ldg(L + e)) - m);
-      z += ex;
-      pnum = fmaf(ex, a_s[e], pnum);
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int e0 = sl * SLAB, ne = min(SLAB, E - e0);
+    __syncthreads();
+    load_slab(logits, t0, T_, E, e0, ne, tile);
+    __syncthreads();
+    if (valid)
+      for (int j = 0; j < ne; ++j) m = fmaxf(m, tile[tid * TS + j]);
+  }
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int e0 = sl * SLAB, ne = min(SLAB, E - e0);
+    if (nslab > 1) {
+      __syncthreads();
+      load_slab(logits, t0, T_, E, e0, ne, tile);
+      __syncthreads();
     }
+    if (valid)
+      for (int j = 0; j < ne; ++j) {
+        const float ex = expf(tile[tid * TS + j] - m);
+        z += ex;
+        pnum = fmaf(ex, a_s[e0 + j], pnum);
+      }
   }
   const float inv = valid ? 1.0f / z : 0.f;
   const float pa = pnum * inv;
@@ -505,58 +545,53 @@ __global__ void __launch_bounds__(256) route_bwd_kernel(
       p1 = gate[t];  // = p[e1]
     }
   }
-  for (int e0 = 0; e0 < E; e0 += 8) {
-    float dl[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u;
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int e0 = sl * SLAB, ne = min(SLAB, E - e0);
+    if (nslab > 1) {
+      __syncthreads();
+      load_slab(logits, t0, T_, E, e0, ne, tile);
+      __syncthreads();
+    }
+    // own row: logits -> dlogits in place (invalid rows -> 0)
+    for (int j = 0; j < ne; ++j) {
+      const int e = e0 + j;
       float v = 0.f;
-      if (valid && e < E) {
-        const float pe = expf(nan_to_ninf(__ldg(L + e)) - m) * inv;
+      if (valid) {
+        const float pe = expf(tile[tid * TS + j] - m) * inv;
         v = d_aux * pe * (a_s[e] - pa);
         if (k == 1) v += gterm * p1 * ((e == e1 ? 1.f : 0.f) - pe);
         else v += (e == e1 ? gterm : 0.f) - (e == e2 ? gterm : 0.f);
       }
-      dl[u] = v;
+      tile[tid * TS + j] = v;
     }
-    if (valid) {
-      if (dl_f32) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (e0 + u < E) dl_f32[t * E + e0 + u] = dl[u];
-      }
-      if (dl_lp) {
-        if (sizeof(LP) == 2 && (ld % 8) == 0 && e0 + 8 <= ld) {
-          uint4 o;
-          o.x = pack_bf16x2(dl[0], dl[1]);
-          o.y = pack_bf16x2(dl[2], dl[3]);
-          o.z = pack_bf16x2(dl[4], dl[5]);
-          o.w = pack_bf16x2(dl[6], dl[7]);
-          *reinterpret_cast<uint4*>(dl_lp + t * ld + e0) = o;
-        } else {
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (e0 + u < ld) dl_lp[t * ld + e0 + u] = (LP)dl[u];
-        }
+    __syncthreads();
+    // row-coalesced write-out; the last slab also zeroes pad columns [E, ld)
+    const int wl = (sl == nslab - 1 && dl_lp) ? max(ne, ld - e0) : ne;
+    for (int r = warp; r < CHUNK; r += RT_THREADS / 32) {
+      const uint64_t tr = t0 + r;
+      if (tr >= T_) break;
+      for (int j = lane; j < wl; j += 32) {
+        const float v = j < ne ? tile[r * TS + j] : 0.f;
+        if (dl_f32 && j < ne) dl_f32[tr * E + e0 + j] = v;
+        if (dl_lp) dl_lp[tr * ld + e0 + j] = (LP)v;
       }
     }
     if (dbg) {
+      // column sums: warp w over its 32 rows, then a fixed order over warps
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        float v = dl[u];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0 && e0 + u < E) atomicAdd(&dbg_s[e0 + u], v);
+      for (int q = 0; q < SLAB / 32; ++q) {
+        float a = 0.f;
+        for (int j = 0; j < 32; ++j) a += tile[(warp * 32 + j) * TS + lane + 32 * q];
+        cs[warp][lane + 32 * q] = a;
+      }
+      __syncthreads();
+      if (tid < ne) {
+        float a = 0.f;
+        for (int w = 0; w < 8; ++w) a += cs[w][tid];
+        atomicAdd(&dbg[e0 + tid], a);
       }
     }
   }
-  if (valid && dl_lp) {
-    const int from = ((E + 7) / 8) * 8;
-    for (int e = from; e < ld; ++e) dl_lp[t * ld + e] = (LP)0.f;
-  }
-  __syncthreads();
-  if (dbg)
-    for (int e = threadIdx.x; e < E; e += blockDim.x) atomicAdd(&dbg[e], dbg_s[e]);
 }
 
 template <typename T>
@@ -715,13 +750,17 @@ void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, con
                     const float* dgate, float d_aux, float* dlogits_f32, void* dlogits_lp,
                     moe_dtype_t lp_dtype, uint32_t ld, float* dbg, cudaStream_t st) {
   if (!T) return;
-  const unsigned blocks = (unsigned)ceil_div(T, 256);
+  const unsigned blocks = (unsigned)ceil_div(T, CHUNK);
+  MOE_CUDA(cudaFuncSetAttribute(route_bwd_kernel<__nv_bfloat16>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, SLAB_SMEM));
+  MOE_CUDA(cudaFuncSetAttribute(route_bwd_kernel<float>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, SLAB_SMEM));
   if (dlogits_lp && lp_dtype == MOE_DTYPE_BF16)
-    route_bwd_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+    route_bwd_kernel<__nv_bfloat16><<<blocks, RT_THREADS, SLAB_SMEM, st>>>(
         T, (int)E, (int)k, logits, expert, gate, keep, count1, dgate, d_aux, dlogits_f32,
         (__nv_bfloat16*)dlogits_lp, (int)ld, dbg);
   else
-    route_bwd_kernel<float><<<blocks, 256, 0, st>>>(T, (int)E, (int)k, logits, expert, gate, keep,
+    route_bwd_kernel<float><<<blocks, RT_THREADS, SLAB_SMEM, st>>>(T, (int)E, (int)k, logits, expert, gate, keep,
                                                     count1, dgate, d_aux, dlogits_f32,
                                                     (float*)dlogits_lp, (int)ld, dbg);
   MOE_LAUNCH_CHECK("route_bwd_kernel");
