@@ -42,7 +42,32 @@ __device__ __forceinline__ float nan_to_ninf(float v) { return isnan(v) ? -INFIN
 // shared memory instead of issuing 32-row-wide scattered global loads.
 __device__ __forceinline__ void load_slab(const float* __restrict__ logits, uint64_t t0, uint64_t T,
                                           int E, int e0, int ne, float* tile) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  if ((E & 3) == 0) {
+    // all 16 float4 loads of a thread in flight before the first store; a
+    // warp instruction covers two 256-byte row pieces
+    constexpr int Q = SLAB / 4;
+    constexpr int PER = CHUNK * Q / RT_THREADS;
+    float4 v[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int x = i * RT_THREADS + tid, r = x / Q, q = x % Q;
+      const uint64_t t = t0 + r;
+      v[i] = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      if (t < T && 4 * q < ne) v[i] = __ldg(reinterpret_cast<const float4*>(logits + t * E + e0) + q);
+    }
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int x = i * RT_THREADS + tid, r = x / Q, q = x % Q;
+      float* d = tile + r * TS + 4 * q;
+      d[0] = nan_to_ninf(v[i].x);
+      d[1] = nan_to_ninf(v[i].y);
+      d[2] = nan_to_ninf(v[i].z);
+      d[3] = nan_to_ninf(v[i].w);
+    }
+    return;
+  }
+  const int warp = tid >> 5, lane = tid & 31;
 #pragma unroll 4
   for (int r = warp; r < CHUNK; r += RT_THREADS / 32) {
     const uint64_t t = t0 + r;
