@@ -546,8 +546,12 @@ void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, con
                             cudaStream_t st) {
   // Three-stream pipeline over double-buffered staging: H2D of step i+1 and
   // D2H of step i-1 overlap the compute of step i (PCIe is full duplex and the
-  // copy engines need no SMs).  The caller's stream waits for this step's D2H,
-  // so y_host / dx_host / the gradients are valid once `st` reaches this call.
+  // copy engines need no SMs).  Input and output stages are released
+  // separately: the H2D of step i+2 only waits for the compute of step i (its
+  // inputs consumed), the compute of step i+2 for the D2H of step i, so in
+  // steady state each copy engine streams back to back and the step time is
+  // max(H2D, compute, D2H).  The caller's stream waits for this step's D2H, so
+  // y_host / dx_host / the gradients are valid once `st` reaches this call.
   const uint64_t bytes = T * dm * esz;
   if (!x_stage) {
     MOE_CUDA(cudaMalloc(&x_stage, 8 * bytes + 64));
@@ -567,11 +571,12 @@ void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, con
   void* dyd = base + bytes;
   void* yd = base + 2 * bytes;
   void* dxd = base + 3 * bytes;
-  if (hp_iter >= 2) MOE_CUDA(cudaStreamWaitEvent(h2d, hp_ev[b][2], 0));  // stage b drained
+  if (hp_iter >= 2) MOE_CUDA(cudaStreamWaitEvent(h2d, hp_ev[b][1], 0));  // inputs b consumed
   MOE_CUDA(cudaMemcpyAsync(xd, x_host, bytes, cudaMemcpyHostToDevice, h2d));
   MOE_CUDA(cudaMemcpyAsync(dyd, dy_host, bytes, cudaMemcpyHostToDevice, h2d));
   MOE_CUDA(cudaEventRecord(hp_ev[b][0], h2d));
   MOE_CUDA(cudaStreamWaitEvent(comp, hp_ev[b][0], 0));
+  if (hp_iter >= 2) MOE_CUDA(cudaStreamWaitEvent(comp, hp_ev[b][2], 0));  // outputs b drained
   forward(w, xd, yd, nullptr, nullptr, nullptr, comp);
   backward(w, dyd, d_aux, dxd, g, comp);
   MOE_CUDA(cudaEventRecord(hp_ev[b][1], comp));
