@@ -176,11 +176,34 @@ def run_reference_arm(args, cfg):
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+# The JSON line is the only thing on stdout: native libraries (NCCL's version
+# banner, CUDA) print to fd 1, so fd 1 is pointed at stderr for the run and the
+# line goes to the saved original stdout.
+_JSON_FD = None
+
+
+def emit(line):
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
+def _redirect_stdout():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
 
 
 # ------------------------------------------------------------------ GPU arm --
 def main():
+    _redirect_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -397,7 +420,7 @@ def main():
         "phases_ms_per_step": {n: v / args.steps for n, v in sorted(phase_tot.items())},
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if ep is not None:
         layer.close()
         ep.close()
