@@ -23,6 +23,8 @@
 #include <cstring>
 #include <mutex>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -848,11 +850,13 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
     ro.El = (int)remote->El;
     ro.Cs = (long long)remote->Cs;
   }
+  const int budget = gemm_cta_budget();
+  const int grid = budget > 0 ? std::min(budget, num_sms()) : num_sms();
   if (CG == 1) {
-    kern<<<num_sms(), THREADS, C_::SMEM, st>>>(ta, tb, tcm, tc2, tax, a, ro);
+    kern<<<grid, THREADS, C_::SMEM, st>>>(ta, tb, tcm, tc2, tax, a, ro);
   } else {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(num_sms() & ~1));
+    cfg.gridDim = dim3((unsigned)std::max(2, grid & ~1));
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = C_::SMEM;
     cfg.stream = st;
@@ -870,6 +874,11 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
 }
 
 }  // namespace tc
+
+int& gemm_cta_budget() {
+  thread_local int budget = 0;
+  return budget;
+}
 
 void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st, const RemoteRows* remote) {
   using namespace tc;

@@ -27,6 +27,16 @@ struct RemoteRows {
   uint64_t Cs;
 };
 
+// Upper bound on the CTAs (SMs) a persistent tcgen05 GEMM launched from this
+// thread may occupy (0: all SMs).  Used to run two GEMMs side by side on
+// disjoint SM sets; set with the scoped GemmCtaBudget.
+int& gemm_cta_budget();
+struct GemmCtaBudget {
+  int saved;
+  explicit GemmCtaBudget(int n) : saved(gemm_cta_budget()) { gemm_cta_budget() = n; }
+  ~GemmCtaBudget() { gemm_cta_budget() = saved; }
+};
+
 // K5: grouped GEMM. bf16 -> tcgen05 (gemm_tc.cu), fp32 -> SIMT FFMA (gemm_simt.cu).
 void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st,
                      const RemoteRows* remote = nullptr);
