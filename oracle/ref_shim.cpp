@@ -7,7 +7,10 @@
 #include <cstring>
 #include <exception>
 #include <stdexcept>
+#include <string>
 #include <vector>
+
+#include <nlohmann/json.hpp>
 
 #include "moesim/collectives.hpp"
 #include "moesim/ring_offload.hpp"
@@ -194,6 +197,46 @@ int ref_ring_simulate(uint32_t layers, uint32_t ring_slots, uint64_t expert_byte
     *baseline_bytes = r.baseline_gpu_bytes;
     return 0;
   } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// workload.cpp:68-85 trace_to_json(...).dump() into out (cap bytes); *len = size.
+int ref_trace_to_json(uint32_t steps, uint32_t ranks, uint32_t experts, uint64_t tokens,
+                      const uint64_t* counts, char* out, uint64_t cap, uint64_t* len) {
+  try {
+    RoutingTrace t;
+    t.steps = steps;
+    t.ranks = ranks;
+    t.experts = experts;
+    t.tokens_per_rank = tokens;
+    t.counts.assign(counts, counts + static_cast<size_t>(steps) * ranks * experts);
+    const std::string s = trace_to_json(t).dump();
+    *len = s.size();
+    if (s.size() + 1 > cap) return 8;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// workload.cpp:87-119 trace_from_json(parse(text)); error text into err.
+int ref_trace_from_json(const char* text, uint32_t* steps, uint32_t* ranks, uint32_t* experts,
+                        uint64_t* tokens, uint64_t* counts, uint64_t counts_cap, char* err,
+                        uint64_t err_cap) {
+  try {
+    const RoutingTrace t = trace_from_json(nlohmann::json::parse(text));
+    *steps = t.steps;
+    *ranks = t.ranks;
+    *experts = t.experts;
+    *tokens = t.tokens_per_rank;
+    if (t.counts.size() > counts_cap) return 8;
+    std::memcpy(counts, t.counts.data(), t.counts.size() * sizeof(uint64_t));
+    return 0;
+  } catch (const std::exception& e) {
+    std::strncpy(err, e.what(), err_cap - 1);
+    err[err_cap - 1] = 0;
     return code_of(std::current_exception());
   }
 }

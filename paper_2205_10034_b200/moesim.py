@@ -8,6 +8,7 @@ reference's value-semantics calling convention).  Chunks are ``bytes``.
 from __future__ import annotations
 
 import ctypes as C
+import json
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -129,6 +130,83 @@ def imbalance_ratio(trace: RoutingTrace) -> float:
     call("moesim_imbalance_ratio", trace.steps, trace.ranks, trace.experts,
          counts.ctypes.data_as(C.c_void_p) if counts.size else None, C.byref(out))
     return out.value
+
+
+def trace_to_json(trace: RoutingTrace) -> str:
+    """workload.cpp:68-85 (schemas/routing_trace.schema.json): the same document
+    the reference's trace_to_json(...).dump() writes — compact, keys sorted."""
+    counts = np.asarray(trace.counts, dtype=np.uint64).reshape(trace.steps, trace.ranks, trace.experts)
+    doc = {"schema_version": 1, "steps": int(trace.steps), "ranks": int(trace.ranks),
+           "experts": int(trace.experts), "tokens_per_rank": int(trace.tokens_per_rank),
+           "counts": counts.astype(np.int64).tolist()}
+    return json.dumps(doc, sort_keys=True, separators=(",", ":"))
+
+
+def trace_from_json(doc) -> RoutingTrace:
+    """workload.cpp:87-119: validate and load a routing trace (str or dict);
+    malformed documents raise ConfigError with the reference's messages."""
+    if isinstance(doc, (str, bytes)):
+        doc = json.loads(doc)
+    for key in ("steps", "ranks", "experts", "tokens_per_rank", "counts"):
+        if key not in doc:
+            raise ConfigError(f"trace.{key}: missing field")
+    steps, ranks, experts = int(doc["steps"]), int(doc["ranks"]), int(doc["experts"])
+    tokens = int(doc["tokens_per_rank"])
+    counts = doc["counts"]
+    out = np.zeros((steps, ranks, experts), dtype=np.uint64)
+    if not isinstance(counts, list) or len(counts) != steps:
+        raise ConfigError("trace.counts: expected one entry per step")
+    for si in range(steps):
+        by_rank = counts[si]
+        if not isinstance(by_rank, list) or len(by_rank) != ranks:
+            raise ConfigError("trace.counts: expected one row per rank")
+        for ri in range(ranks):
+            row = by_rank[ri]
+            if not isinstance(row, list) or len(row) != experts:
+                raise ConfigError("trace.counts: expected one count per expert")
+            out[si, ri, :] = row
+            if sum(int(v) for v in row) != tokens:
+                raise ConfigError("trace.counts: row sum does not match tokens_per_rank")
+    return RoutingTrace(steps, ranks, experts, tokens, out)
+
+
+class RoutingTraceRecorder:
+    """Measured routing -> RoutingTrace: per step, the device
+    routing's pre-drop assignment counts (count1 + count2 of moe_route /
+    moe_layer_forward) are appended on the device, so recording adds no host
+    synchronisation; `trace()` gathers all EP ranks (rank order) and returns the
+    reference's [step][rank][expert] trace that `WorkloadConfig::trace_file`
+    (scenario.cpp:67-80) can replay. tokens_per_rank = k * T (every token is
+    routed k times)."""
+
+    def __init__(self, experts: int, tokens: int, top_k: int, max_steps: int, device=None):
+        import torch
+        self.E, self.T, self.k = experts, tokens, top_k
+        self.buf = torch.zeros(max_steps, experts, dtype=torch.int64, device=device or "cuda")
+        self.steps = 0
+
+    def record(self, routing) -> None:
+        """routing: the dict returned by MoELayer.forward(..., routing=True) or route()."""
+        if self.steps >= self.buf.shape[0]:
+            raise ConfigError("trace.steps: recorder is full")
+        c = routing["count1"].to(self.buf.dtype)
+        if self.k == 2:
+            c = c + routing["count2"].to(self.buf.dtype)
+        self.buf[self.steps].copy_(c, non_blocking=True)
+        self.steps += 1
+
+    def trace(self, group=None) -> RoutingTrace:
+        import torch
+        import torch.distributed as dist
+        mine = self.buf[: self.steps]
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            parts = [torch.empty_like(mine) for _ in range(dist.get_world_size(group))]
+            dist.all_gather(parts, mine, group=group)
+            allr = torch.stack(parts, dim=1)  # [step][rank][expert]
+        else:
+            allr = mine.unsqueeze(1)
+        counts = allr.cpu().numpy().astype(np.uint64)
+        return RoutingTrace(self.steps, counts.shape[1], self.E, self.k * self.T, counts)
 
 
 LOAD, COMPUTE, RELEASE = 0, 1, 2

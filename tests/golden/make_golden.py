@@ -113,6 +113,33 @@ def ref_simulate(layers, slots, expert_bytes, dense_bytes, compute_ns, bw, lat):
             "copy_ns": cp.value, "peak_bytes": pk.value, "baseline_bytes": bl.value}
 
 
+def ref_trace_to_json(steps, ranks, experts, tokens, counts):
+    r = oracle.ref()
+    c = np.ascontiguousarray(np.asarray(counts, dtype=np.uint64).reshape(-1))
+    buf = C.create_string_buffer(1 << 22)
+    n = C.c_uint64(0)
+    rc = r.ref_trace_to_json(C.c_uint32(steps), C.c_uint32(ranks), C.c_uint32(experts),
+                             C.c_uint64(tokens), oracle.P(c) if c.size else None, buf,
+                             C.c_uint64(len(buf)), C.byref(n))
+    assert rc == 0, rc
+    return buf.value.decode()
+
+
+def ref_trace_from_json(text):
+    r = oracle.ref()
+    st, rk, ex = C.c_uint32(0), C.c_uint32(0), C.c_uint32(0)
+    tok = C.c_uint64(0)
+    counts = np.zeros(1 << 16, dtype=np.uint64)
+    err = C.create_string_buffer(512)
+    rc = r.ref_trace_from_json(text.encode(), C.byref(st), C.byref(rk), C.byref(ex), C.byref(tok),
+                               oracle.P(counts), C.c_uint64(counts.size), err, C.c_uint64(512))
+    if rc:
+        return {"error": rc, "message": err.value.decode()}
+    n = st.value * rk.value * ex.value
+    return {"steps": st.value, "ranks": rk.value, "experts": ex.value, "tokens_per_rank": tok.value,
+            "counts": counts[:n].astype(np.int64).tolist()}
+
+
 def main():
     assert oracle.ref() is not None, "build the reference first: make -C oracle ref"
     gold = {"source": "oracle/_ref/libmoesim_ref.so built from /root/reference/proj (see oracle/Makefile)"}
@@ -189,6 +216,23 @@ def main():
     ]
     gold["ring_simulate"] = [{"args": list(a[:4]) + [a[4], a[5], a[6]],
                               "expected": ref_simulate(*a)} for a in sims]
+
+    # workload.cpp:68-119 — routing-trace JSON (schemas/routing_trace.schema.json)
+    tj = []
+    for args in ((7, 1, 2, 4, 100, 0.0), (11, 3, 2, 8, 64, 1.2), (5, 2, 3, 5, 33, 0.7)):
+        c = oracle.gen_trace(*args, which="ref")
+        tj.append({"args": list(args), "json": ref_trace_to_json(args[1], args[2], args[3], args[4], c)})
+    tj.append({"args": [0, 0, 1, 1, 0, 0.0], "json": ref_trace_to_json(0, 1, 1, 0, [])})
+    gold["trace_to_json"] = tj
+    bad = [
+        '{"steps":1,"ranks":1,"experts":2,"counts":[[[1,1]]]}',                         # missing tokens
+        '{"steps":2,"ranks":1,"experts":2,"tokens_per_rank":2,"counts":[[[1,1]]]}',     # steps
+        '{"steps":1,"ranks":2,"experts":2,"tokens_per_rank":2,"counts":[[[1,1]]]}',     # ranks
+        '{"steps":1,"ranks":1,"experts":3,"tokens_per_rank":2,"counts":[[[1,1]]]}',     # experts
+        '{"steps":1,"ranks":1,"experts":2,"tokens_per_rank":3,"counts":[[[1,1]]]}',     # row sum
+        '{"steps":1,"ranks":1,"experts":2,"tokens_per_rank":2,"counts":[[[2,0]]],"schema_version":1}',
+    ]
+    gold["trace_from_json"] = [{"json": t, "expected": ref_trace_from_json(t)} for t in bad]
 
     with open(os.path.join(OUT, "reference_golden.json"), "w") as f:
         json.dump(gold, f, indent=1, sort_keys=True)

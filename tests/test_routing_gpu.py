@@ -80,3 +80,23 @@ def test_routing_zero_capacity():
     got, ref = run_both(L, 2, 0)
     check(got, ref, 600)
     assert got["keep"].sum() == 0
+
+
+def test_routing_trace_recorder_matches_device_counts():
+    """measured routing exported as the reference's RoutingTrace
+    JSON; trace_from_json re-validates every row sum (= k*T pre-drop assignments)."""
+    from paper_2205_10034_b200 import moesim
+    from paper_2205_10034_b200.layer import capacity, route
+    E, k, T = 16, 2, 4096
+    rec = moesim.RoutingTraceRecorder(E, T, k, max_steps=3)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    expect = []
+    for _ in range(3):
+        logits = torch.randn(T, E, device="cuda", generator=g)
+        r = route(logits, k, capacity(k, 1.25, T, E))
+        rec.record(r)
+        expect.append((r["count1"].long() + r["count2"].long()).cpu().tolist())
+    back = moesim.trace_from_json(moesim.trace_to_json(rec.trace()))
+    assert (back.steps, back.ranks, back.experts, back.tokens_per_rank) == (3, 1, E, k * T)
+    for s in range(3):
+        assert back.counts[s, 0].tolist() == expect[s]
