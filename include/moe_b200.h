@@ -315,6 +315,32 @@ moe_status_t moe_comm_destroy(void* comm);
 moe_status_t moe_alltoall_packed(void* comm, const void* send, void* recv, uint64_t bytes_per_peer,
                                  uint32_t slices_per_peer, int fused, void* stream);
 
+/* Gradient-bucket fusion for replicated parameters (the gates of a stack of
+ * MoE layers).  Replaces GradBucket / make_gradient_buckets
+ * (collectives.hpp:80-109, collectives.cpp:120-162): the n parameter ids are
+ * registered in REVERSE layer order into buckets of at most `capacity`; a
+ * bucket flushes exactly once, when its last gradient is pushed, with its
+ * payload in registration order.  On the device a flush packs the bucket's
+ * fp32 gradients into one flat buffer, issues ONE ncclAllReduce(sum) over
+ * `comm` and unpacks them multiplied by `scale` (e.g. 1/world for a mean) — on
+ * the stream passed to push, no host synchronisation.  grads/numel may both be
+ * NULL (bookkeeping only); comm may be NULL (one rank).  Errors:
+ * INVALID_ARGUMENT for capacity 0, a duplicate push or an unknown id. */
+typedef struct moe_grad_buckets* moe_grad_buckets_t;
+moe_status_t moe_grad_buckets_create(void* comm, uint32_t n, const uint64_t* ids_layer_order,
+                                     void* const* grads, const uint64_t* numel,
+                                     uint32_t capacity, float scale, moe_grad_buckets_t* out);
+moe_status_t moe_grad_buckets_destroy(moe_grad_buckets_t b);
+/* *flushed = index of the bucket this push completed (its all-reduce is
+ * enqueued on stream), or -1 while the bucket is still held. */
+moe_status_t moe_grad_buckets_push(moe_grad_buckets_t b, uint64_t id, void* stream,
+                                   int32_t* flushed);
+moe_status_t moe_grad_buckets_reset(moe_grad_buckets_t b);
+uint32_t moe_grad_buckets_count(moe_grad_buckets_t b);
+/* ids of bucket i in registration order (capacity entries max); *n = count */
+moe_status_t moe_grad_buckets_ids(moe_grad_buckets_t b, uint32_t i, uint64_t* ids,
+                                  uint32_t capacity, uint32_t* n);
+
 /* ======================================================================
  * 4. ring-of-sections inference (K7)
  * ====================================================================== */

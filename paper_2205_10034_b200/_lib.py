@@ -203,6 +203,12 @@ SIGNATURES = {
     "moe_comm_create": (_I, [_VP, _U32, _U32, C.POINTER(_VP)]),
     "moe_comm_destroy": (_I, [_VP]),
     "moe_alltoall_packed": (_I, [_VP, _VP, _VP, _U64, _U32, _I, _VP]),
+    "moe_grad_buckets_create": (_I, [_VP, _U32, _VP, _VP, _VP, _U32, C.c_float, C.POINTER(_VP)]),
+    "moe_grad_buckets_destroy": (_I, [_VP]),
+    "moe_grad_buckets_push": (_I, [_VP, _U64, _VP, C.POINTER(C.c_int32)]),
+    "moe_grad_buckets_reset": (_I, [_VP]),
+    "moe_grad_buckets_count": (_U32, [_VP]),
+    "moe_grad_buckets_ids": (_I, [_VP, _U32, _VP, _U32, C.POINTER(_U32)]),
     "moe_ring_create": (_I, [_VP, C.POINTER(RingDesc), C.POINTER(_VP)]),
     "moe_ring_destroy": (_I, [_VP]),
     "moe_ring_section_bytes": (_U64, [_VP]),

@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 
+#include "buckets.h"
 #include "common.cuh"
 #include "kernels.h"
 #include "layer.h"
@@ -382,6 +383,52 @@ moe_status_t moe_alltoall_packed(void* comm, const void* send, void* recv, uint6
   return guard([&] {
     moe::arg_check(comm != nullptr, "alltoall.comm: must be non-null");
     moe::alltoall_packed(comm, send, recv, bytes_per_peer, slices_per_peer, fused, S(stream));
+  });
+}
+
+// ----------------------------------------------------------- buckets -----
+moe_status_t moe_grad_buckets_create(void* comm, uint32_t n, const uint64_t* ids_layer_order,
+                                     void* const* grads, const uint64_t* numel,
+                                     uint32_t capacity, float scale, moe_grad_buckets_t* out) {
+  return guard([&] {
+    moe::arg_check(out != nullptr, "bucket: out must be non-null");
+    *out = reinterpret_cast<moe_grad_buckets_t>(
+        new moe::GradBuckets(comm, n, ids_layer_order, grads, numel, capacity, scale));
+  });
+}
+
+moe_status_t moe_grad_buckets_destroy(moe_grad_buckets_t b) {
+  return guard([&] { delete reinterpret_cast<moe::GradBuckets*>(b); });
+}
+
+moe_status_t moe_grad_buckets_push(moe_grad_buckets_t b, uint64_t id, void* stream,
+                                   int32_t* flushed) {
+  return guard([&] {
+    moe::arg_check(b != nullptr && flushed != nullptr, "bucket: null argument");
+    *flushed = reinterpret_cast<moe::GradBuckets*>(b)->push(id, S(stream));
+  });
+}
+
+moe_status_t moe_grad_buckets_reset(moe_grad_buckets_t b) {
+  return guard([&] {
+    moe::arg_check(b != nullptr, "bucket: null argument");
+    reinterpret_cast<moe::GradBuckets*>(b)->reset();
+  });
+}
+
+uint32_t moe_grad_buckets_count(moe_grad_buckets_t b) {
+  return b ? reinterpret_cast<moe::GradBuckets*>(b)->count() : 0;
+}
+
+moe_status_t moe_grad_buckets_ids(moe_grad_buckets_t b, uint32_t i, uint64_t* ids,
+                                  uint32_t capacity, uint32_t* n) {
+  return guard([&] {
+    auto* g = reinterpret_cast<moe::GradBuckets*>(b);
+    moe::arg_check(g != nullptr && n != nullptr, "bucket: null argument");
+    if (i >= g->count()) moe::fail(MOE_ERR_OUT_OF_RANGE, "bucket: index out of range");
+    const auto& v = g->ids(i);
+    *n = (uint32_t)v.size();
+    for (uint32_t q = 0; q < v.size() && q < capacity; ++q) ids[q] = v[q];
   });
 }
 

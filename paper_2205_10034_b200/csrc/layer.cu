@@ -28,15 +28,10 @@
 #include "kernels.h"
 #include "ep_p2p.h"
 #include "layer.h"
+#include "nccl_check.h"
 
 namespace moe {
 
-#define MOE_NCCL(expr)                                                                  \
-  do {                                                                                  \
-    ncclResult_t _r = (expr);                                                           \
-    if (_r != ncclSuccess)                                                              \
-      ::moe::fail(MOE_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));    \
-  } while (0)
 
 namespace {
 

@@ -209,6 +209,64 @@ class RoutingTraceRecorder:
         return RoutingTrace(self.steps, counts.shape[1], self.E, self.k * self.T, counts)
 
 
+class GradBuckets:
+    """Gradient-bucket fusion (moe_grad_buckets_*) with the
+    semantics of make_gradient_buckets + GradBucket (collectives.cpp:120-162):
+    ids in layer order are registered in reverse into buckets of <= capacity;
+    push(id) returns the bucket index it flushed (ids in registration order via
+    ids(b)) or None while held.  With `grads` (fp32 device tensors, same order
+    as ids) a flush packs, all-reduces over `ep` (NCCL) and unpacks x `scale`
+    on the stream; without, it is bookkeeping only (CPU-usable)."""
+
+    def __init__(self, ids_layer_order: Sequence[int], capacity: int, grads=None, ep=None,
+                 scale: float = 1.0):
+        n = len(ids_layer_order)
+        self._ids = (C.c_uint64 * max(n, 1))(*ids_layer_order)
+        gp = nm = None
+        self._grads = list(grads) if grads is not None else None
+        if grads is not None:
+            assert len(grads) == n
+            for g in grads:
+                assert g.dtype.is_floating_point and g.element_size() == 4 and g.is_contiguous()
+            gp = (C.c_void_p * max(n, 1))(*[g.data_ptr() for g in grads])
+            nm = (C.c_uint64 * max(n, 1))(*[g.numel() for g in grads])
+        h = C.c_void_p()
+        call("moe_grad_buckets_create", ep.comm if ep is not None else None, n,
+             C.cast(self._ids, C.c_void_p), C.cast(gp, C.c_void_p) if gp else None,
+             C.cast(nm, C.c_void_p) if nm else None, capacity, float(scale), C.byref(h))
+        self._h = h
+
+    def __len__(self) -> int:
+        return int(lib.moe_grad_buckets_count(self._h))
+
+    def ids(self, b: int) -> List[int]:
+        out = (C.c_uint64 * 4096)()
+        n = C.c_uint32(0)
+        call("moe_grad_buckets_ids", self._h, b, C.cast(out, C.c_void_p), 4096, C.byref(n))
+        return [int(out[i]) for i in range(n.value)]
+
+    def push(self, grad_id: int, stream=None) -> Optional[int]:
+        from .layer import _stream
+        f = C.c_int32(-1)
+        call("moe_grad_buckets_push", self._h, grad_id,
+             _stream(stream) if self._grads is not None else None, C.byref(f))
+        return None if f.value < 0 else int(f.value)
+
+    def reset(self) -> None:
+        call("moe_grad_buckets_reset", self._h)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            call("moe_grad_buckets_destroy", self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 LOAD, COMPUTE, RELEASE = 0, 1, 2
 
 

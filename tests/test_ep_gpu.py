@@ -51,6 +51,25 @@ def _worker(rank, world, port, case, q):
                     assert torch.equal(recv[s * nn:(s + 1) * nn], allsend[s][rank * n:rank * n + nn])
             q.put((rank, "ok"))
             return
+        if case == "buckets":
+            # gradient-bucket fusion: 5 fp32 "gate gradients" of different
+            # sizes, rank-dependent values, pushed in a rank-dependent order;
+            # each flush all-reduces its bucket once (sum x scale)
+            from paper_2205_10034_b200.moesim import GradBuckets
+            sizes = [1000, 3, 64 * 1024, 7, 4096]
+            grads = [torch.full((n,), float(rank + 1) * (i + 1), device="cuda")
+                     for i, n in enumerate(sizes)]
+            gb = GradBuckets(list(range(10, 15)), 2, grads=grads, ep=ep, scale=0.5)
+            order = [14, 13, 12, 11, 10] if rank == 0 else [13, 14, 11, 12, 10]
+            flushed = [gb.push(i) for i in order]
+            assert [f for f in flushed if f is not None] == [0, 1, 2], flushed
+            torch.cuda.synchronize()
+            tot = sum(r + 1 for r in range(world))
+            for i, g in enumerate(grads):
+                assert torch.all(g == 0.5 * tot * (i + 1)), (i, g[:4])
+            gb.close()
+            q.put((rank, "ok"))
+            return
         E, k, d, dff, T, dt, exch = case
         cfg = MoEConfig(E, k, d, dff, 1.25, T, dt, exchange=exch)
         lep = MoELayer(cfg, ep=ep)
@@ -110,6 +129,10 @@ def _run(case, world=2):
 
 def test_packed_alltoall_fused_and_unfused():
     _run("a2a")
+
+
+def test_gradient_buckets_allreduce():
+    _run("buckets")
 
 
 @pytest.mark.parametrize("case", [

@@ -200,3 +200,16 @@ def test_train_step_host_pipeline_matches_device_calls():
         assert torch.equal(hy[i], ref[i][0]) and torch.equal(hdx[i], ref[i][1]), i
     err = (layer.grads["dw1"].cpu() - ref[2][2]).abs().max() / ref[2][2].abs().max()
     assert err < 1e-5
+
+
+def test_gradient_buckets_single_rank_scale():
+    """moe_grad_buckets on one rank (no communicator): flushes follow the
+    reverse-layer registration; only the scale is applied."""
+    from paper_2205_10034_b200.moesim import GradBuckets
+    grads = [torch.full((n,), float(i + 1), device="cuda") for i, n in enumerate([5, 4096, 33])]
+    gb = GradBuckets([1, 2, 3], 2, grads=grads, scale=0.25)
+    assert gb.push(3) is None and gb.push(2) == 0 and gb.push(1) == 1
+    torch.cuda.synchronize()
+    for i, g in enumerate(grads):
+        assert torch.all(g == 0.25 * (i + 1))
+    gb.close()
