@@ -201,6 +201,30 @@ def _redirect_stdout():
     os.dup2(2, 1)
 
 
+ALL_CPUS = os.sched_getaffinity(0)
+
+
+def bind_to_gpu_numa(local):
+    """Pin this rank to the CPU cores NVML reports as local to its GPU, so the
+    pinned host buffers of the host-buffer (e2e) path are first-touched on the
+    GPU's NUMA node and DMA does not cross the socket interconnect."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        idx = int(vis.split(",")[local]) if vis else local
+        h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        pass
+    return None
+
+
 # ------------------------------------------------------------------ GPU arm --
 def main():
     _redirect_stdout()
@@ -231,6 +255,7 @@ def main():
 
     ws, rank, local = dist_env()
     assert args.gpus == ws or ws == 1, "--gpus must match WORLD_SIZE"
+    numa_cpus = bind_to_gpu_numa(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ep = None
@@ -354,10 +379,12 @@ def main():
         e2e = {"value": ws * T * args.steps / (e_ms / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
                "ms_per_step": e_ms / args.steps,
-               "api": "moe_layer_train_step_host (pinned x, dy -> y, dx)"}
+               "api": "moe_layer_train_step_host (pinned x, dy -> y, dx)",
+               "host_cpus_bound": numa_cpus}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
+        os.sched_setaffinity(0, ALL_CPUS)  # the CPU baseline gets every host core
         import oracle
         n = cpu_sample_tokens(cfg)
         v, dt = cpu_oracle_tokens_per_s(cfg, n)
