@@ -16,7 +16,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmoe_b200.so")
+# MOE_B200_LIB: load another build of the same ABI (A/B benchmarking only)
+LIB_PATH = os.environ.get("MOE_B200_LIB") or os.path.join(_HERE, "libmoe_b200.so")
 
 MOE_OK = 0
 MOE_ERR_INVALID_ARGUMENT = 1

@@ -124,8 +124,11 @@ __device__ __forceinline__ int src_offset(const int32_t* cnt, uint32_t E, uint32
 
 constexpr int MAXE = 256;
 
-// grid: ceil(T/8) blocks, warp per token
-template <typename T>
+// Persistent grid (a few blocks per SM), warp per token, grid-stride: the
+// count-matrix prologue and the system-scope fence of the completion signal
+// are paid once per block instead of once per 8 tokens, and each lane has all
+// 16-byte pieces of its row in flight before the first (remote) store.
+template <typename T, int NV>
 __global__ void __launch_bounds__(256) p2p_dispatch_kernel(
     Win w, uint32_t* ctr, uint64_t T_, int d, int k, uint64_t C, const T* __restrict__ x,
     const int32_t* __restrict__ expert, const int32_t* __restrict__ position,
@@ -134,10 +137,11 @@ __global__ void __launch_bounds__(256) p2p_dispatch_kernel(
   const int32_t* cnt = cnt_of(w);
   for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) off_s[e] = src_offset(cnt, w.E, w.me, e);
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int nv = (int)(w.row_bytes / 16);
-  const uint64_t t = blockIdx.x * 8ull + warp;
-  if (t < T_) {
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T_;
+       t += nwarps) {
     uint4* dst[2] = {nullptr, nullptr};
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
@@ -153,10 +157,21 @@ __global__ void __launch_bounds__(256) p2p_dispatch_kernel(
       }
     }
     const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
-    for (int v = lane; v < nv; v += 32) {
-      const uint4 val = __ldg(src + v);
-      if (dst[0]) dst[0][v] = val;
-      if (dst[1]) dst[1][v] = val;
+    if constexpr (NV > 0) {
+      uint4 val[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) val[q] = __ldg(src + lane + 32 * q);
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        if (dst[0]) dst[0][lane + 32 * q] = val[q];
+        if (dst[1]) dst[1][lane + 32 * q] = val[q];
+      }
+    } else {  // any row size
+      for (int v = lane; v < nv; v += 32) {
+        const uint4 val = __ldg(src + v);
+        if (dst[0]) dst[0][v] = val;
+        if (dst[1]) dst[1][v] = val;
+      }
     }
   }
   grid_done_signal(w, ctr, SLOT_DISPATCH, epoch);
@@ -227,10 +242,11 @@ __global__ void __launch_bounds__(256) p2p_combine_bwd_kernel(
   const int32_t* cnt = cnt_of(w);
   for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) off_s[e] = src_offset(cnt, w.E, w.me, e);
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const T* Yh = reinterpret_cast<const T*>(w.peers[w.me] + off_yh);
-  const uint64_t t = blockIdx.x * 8ull + warp;
-  if (t < T_) {
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T_;
+       t += nwarps) {
     for (int i = 0; i < k; ++i) {
       const int32_t s = slot[t * k + i];
       if (s < 0) {
@@ -389,16 +405,27 @@ void p2p_counts(const P2PWindow& w, const int32_t* kept, uint64_t epoch, cudaStr
   count_launch();
 }
 
+unsigned persistent_grid(uint64_t T) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(T, 8), (uint64_t)num_sms() * 4));
+}
+
 void p2p_dispatch(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t k, uint64_t C,
                   moe_dtype_t dt, const void* x, const int32_t* expert, const int32_t* position,
                   int32_t* slot, uint64_t epoch, cudaStream_t st) {
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, ceil_div(T, 8));
-  if (dt == MOE_DTYPE_BF16)
-    p2p_dispatch_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-        win_of(w), ctr_of(w, 0), T, d, k, C, (const __nv_bfloat16*)x, expert, position, slot, epoch);
-  else
-    p2p_dispatch_kernel<float><<<grid, 256, 0, st>>>(win_of(w), ctr_of(w, 0), T, d, k, C,
-                                                     (const float*)x, expert, position, slot, epoch);
+  const unsigned grid = persistent_grid(T);
+  const bool v4 = w.row_bytes == 4 * 512;  // d = 1024 bf16 / 512 fp32: 4 pieces per lane
+  if (dt == MOE_DTYPE_BF16) {
+    if (v4)
+      p2p_dispatch_kernel<__nv_bfloat16, 4><<<grid, 256, 0, st>>>(
+          win_of(w), ctr_of(w, 0), T, d, k, C, (const __nv_bfloat16*)x, expert, position, slot, epoch);
+    else
+      p2p_dispatch_kernel<__nv_bfloat16, 0><<<grid, 256, 0, st>>>(
+          win_of(w), ctr_of(w, 0), T, d, k, C, (const __nv_bfloat16*)x, expert, position, slot, epoch);
+  } else {
+    p2p_dispatch_kernel<float, 0><<<grid, 256, 0, st>>>(win_of(w), ctr_of(w, 0), T, d, k, C,
+                                                        (const float*)x, expert, position, slot,
+                                                        epoch);
+  }
   MOE_LAUNCH_CHECK("p2p_dispatch_kernel");
   count_launch();
 }
@@ -414,7 +441,7 @@ void p2p_combine_bwd(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t k, moe
                      const void* dy, const int32_t* slot, const float* gate,
                      const int32_t* expert, const int32_t* position, float* dgate, uint64_t epoch,
                      cudaStream_t st) {
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, ceil_div(T, 8));
+  const unsigned grid = persistent_grid(T);
   if (dt == MOE_DTYPE_BF16)
     p2p_combine_bwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
         win_of(w), w.off_yh, ctr_of(w, 1), T, d, k, (const __nv_bfloat16*)dy, slot, gate, expert,

@@ -377,7 +377,18 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 9) {
     // ================= MMA issuer (leader CTA only when paired) =================
-    if (lane == 0 && crank == 0) {
+    // Two issue loops, chosen per instantiation by measurement (A/B on one
+    // B200): with a heavy epilogue (GeLU, GeLU', fp32 outputs) the whole warp
+    // walks the loop in uniform control flow and one elected lane issues (the
+    // descriptors stay in uniform registers, ~4x fewer instructions per K
+    // block, which matters when the epilogue warps compete for issue slots);
+    // with a light epilogue a single lane runs the loop (measured ~5% faster
+    // for the K = 4096 GEMMs).  Per 64-wide K block: 4 MMAs whose descriptors
+    // differ by a constant (+32 B K-major, +2 KiB MN-major start address).
+    constexpr bool kWarpIssue = EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU || CF32;
+    constexpr uint64_t ADV_A = A_MN ? (2048 >> 4) : (32 >> 4);
+    constexpr uint64_t ADV_B = B_MN ? (2048 >> 4) : (32 >> 4);
+    if (crank == 0 && (kWarpIssue || lane == 0)) {
       uint32_t it = 0, tcount = 0;
       for (int w = unit; w < total_work; w += nunits, ++tcount) {
         int g, mb, nb;
@@ -394,20 +405,25 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc_fence_after();
           const uint32_t aBase = smem_u32(smem + s * C_::STAGE_BYTES);
           const uint32_t bBase = aBase + C_::A_BYTES;
+          const uint64_t da0 = A_MN ? umma_desc_sw128(aBase, 8192, 1024) : umma_desc_sw128(aBase, 16, 1024);
+          const uint64_t db0 = B_MN ? umma_desc_sw128(bBase, 8192, 1024) : umma_desc_sw128(bBase, 16, 1024);
+          if (!kWarpIssue || elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t da = A_MN ? umma_desc_sw128(aBase + kk * 2048, 8192, 1024)
-                                     : umma_desc_sw128(aBase + kk * 32, 16, 1024);
-            const uint64_t db = B_MN ? umma_desc_sw128(bBase + kk * 2048, 8192, 1024)
-                                     : umma_desc_sw128(bBase + kk * 32, 16, 1024);
-            if (CG == 2) tc_mma_bf16_2sm(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
-            else tc_mma_bf16(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint32_t accum = (kb | kk) != 0 ? 1u : 0u;
+              if (CG == 2) tc_mma_bf16_2sm(d_tmem, da0 + kk * ADV_A, db0 + kk * ADV_B, idesc, accum);
+              else tc_mma_bf16(d_tmem, da0 + kk * ADV_A, db0 + kk * ADV_B, idesc, accum);
+            }
+            if (CG == 2) tc_commit_2sm_mc(&empty[s], 0x3);
+            else tc_commit(&empty[s]);
           }
-          if (CG == 2) tc_commit_2sm_mc(&empty[s], 0x3);
-          else tc_commit(&empty[s]);
+          if (kWarpIssue) __syncwarp();
         }
-        if (CG == 2) tc_commit_2sm_mc(&tfull[acc], 0x3);
-        else tc_commit(&tfull[acc]);
+        if (!kWarpIssue || elect_one()) {
+          if (CG == 2) tc_commit_2sm_mc(&tfull[acc], 0x3);
+          else tc_commit(&tfull[acc]);
+        }
+        if (kWarpIssue) __syncwarp();
       }
     }
   } else if (warp < EPI_WARPS) {

@@ -352,23 +352,34 @@ __global__ void dispatch_kernel(uint64_t T_, int d, int E, int k, uint64_t Cs, u
                                 const int32_t* __restrict__ position, T* __restrict__ buf,
                                 int32_t* __restrict__ slot) {
   const int lane = threadIdx.x & 31;
-  const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (t >= T_) return;
-  int64_t dst[2] = {-1, -1};
-  for (int i = 0; i < k; ++i) {
-    const int e = expert[t * k + i];
-    const int p = position[t * k + i];
-    const int64_t s = ((uint64_t)p < C) ? (int64_t)e * (int64_t)Cs + p : -1;
-    dst[i] = s;
-    if (lane == 0) slot[t * k + i] = (int32_t)s;
-  }
-  if (dst[0] < 0 && dst[1] < 0) return;
-  const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
-  const int nv = d / Vec<T>::N;
-  for (int v = lane; v < nv; v += 32) {
-    const uint4 val = __ldg(src + v);
-    for (int i = 0; i < k; ++i)
-      if (dst[i] >= 0) reinterpret_cast<uint4*>(buf + dst[i] * d)[v] = val;
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T_;
+       t += nwarps) {
+    int64_t dst[2] = {-1, -1};
+    for (int i = 0; i < k; ++i) {
+      const int e = expert[t * k + i];
+      const int p = position[t * k + i];
+      const int64_t s = ((uint64_t)p < C) ? (int64_t)e * (int64_t)Cs + p : -1;
+      dst[i] = s;
+      if (lane == 0) slot[t * k + i] = (int32_t)s;
+    }
+    if (dst[0] < 0 && dst[1] < 0) continue;
+    const uint4* src = reinterpret_cast<const uint4*>(x + t * d);
+    const int nv = d / Vec<T>::N;
+    constexpr int B = 4;  // 16-byte pieces per lane in flight
+    for (int v0 = 0; v0 < nv; v0 += 32 * B) {
+      uint4 val[B];
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if (v0 + lane + 32 * q < nv) val[q] = __ldg(src + v0 + lane + 32 * q);
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        const int v = v0 + lane + 32 * q;
+        if (v >= nv) continue;
+        for (int i = 0; i < k; ++i)
+          if (dst[i] >= 0) reinterpret_cast<uint4*>(buf + dst[i] * d)[v] = val[q];
+      }
+    }
   }
 }
 
@@ -694,7 +705,7 @@ void dispatch_tokens(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C,
                      moe_dtype_t dt, const void* x, const int32_t* expert, const int32_t* position,
                      const int32_t* kept, void* buf, int32_t* slot, cudaStream_t st) {
   const uint64_t Cs = round_up(C, pad);
-  const unsigned blocks = (unsigned)ceil_div(T, 8);
+  const unsigned blocks = (unsigned)std::min<uint64_t>(ceil_div(T, 8), (uint64_t)num_sms() * 8);
   if (T) {
     if (dt == MOE_DTYPE_BF16)
       dispatch_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
