@@ -117,6 +117,33 @@ def test_tc_ragged_m_gelu():
     assert_close(got2, ref2, 1e-2)
 
 
+def test_tc_gelu_large_preactivations():
+    """GeLU epilogue far into both tails (|h| up to ~40): gelu -> h / 0, gelu' ->
+    1 / 0, no NaN (the epilogue's quartic is clamped; SURVEY Appendix A act = erf-GeLU)."""
+    torch.manual_seed(5)
+    M, N, K = 256, 512, 64
+    A = (torch.rand(M, K, device=dev) * 2 - 1).to(torch.bfloat16)
+    W = ((torch.rand(1, N, K, device=dev) * 2 - 1) * 4.0).to(torch.bfloat16)  # |h| up to ~50
+    Cm = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+    C2 = torch.empty_like(Cm)
+    m, a_row, b = i32([M]), i32([0]), i32([0])
+    p = GemmProblem()
+    p.kind, p.epilogue = _lib.MOE_GEMM_RAGGED_M, _lib.MOE_EPI_GELU
+    p.dtype_ab = p.dtype_c = _lib.MOE_DTYPE_BF16
+    p.groups, p.N, p.K, p.a_rows, p.num_b = 1, N, K, M, 1
+    p.m, p.a_row, p.c_row, p.b = m.data_ptr(), a_row.data_ptr(), a_row.data_ptr(), b.data_ptr()
+    p.A, p.B, p.C, p.C2 = A.data_ptr(), W.data_ptr(), Cm.data_ptr(), C2.data_ptr()
+    p.ldc = N
+    grouped_gemm(p)
+    torch.cuda.synchronize()
+    h = A.float() @ W[0].float().t()
+    assert h.abs().max() > 20
+    act, grad = Cm.float(), C2.float()
+    assert torch.isfinite(act).all() and torch.isfinite(grad).all()
+    assert ((act - gelu(h)).abs() <= 1e-2 * h.abs().clamp_min(1)).all()
+    assert ((grad - gelu_grad(h)).abs() <= 1.5e-2).all()
+
+
 def test_tc_ragged_m_dgelu_with_colsum():
     got, ref, cs, ref_cs = ragged_m_case(torch.bfloat16, True, _lib.MOE_EPI_DGELU, bias=False,
                                          colsum=True)

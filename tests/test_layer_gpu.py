@@ -154,7 +154,8 @@ def torch_reference(layer, x, dy, rout, d_aux):
     return y.detach(), xf.grad, wg.grad, w1.grad, b1.grad, w2.grad, b2.grad
 
 
-@pytest.mark.parametrize("E,k,d,dff,T", [(64, 1, 1024, 4096, 65536), (32, 2, 1024, 4096, 16384)])
+@pytest.mark.parametrize("E,k,d,dff,T", [(64, 1, 1024, 4096, 65536), (32, 2, 1024, 4096, 16384),
+                                         (16, 2, 4096, 16384, 4096)])  # last: c4 layer widths
 def test_layer_full_size_vs_torch_fp32(E, k, d, dff, T):
     cfg = MoEConfig(E, k, d, dff, 1.25, T, torch.bfloat16)
     layer = MoELayer(cfg)
