@@ -346,11 +346,31 @@ struct Vec<float> {
   static constexpr int N = 4;
 };
 
+// Zero rows [kept_e, round_up(kept_e, pad)) of expert e's slot region (the
+// weight-gradient GEMM runs whole K blocks); block-strided over experts.
+template <typename T>
+__device__ __forceinline__ void zero_pad_rows(int d, int E, uint64_t Cs, uint32_t pad,
+                                              const int32_t* __restrict__ kept, T* __restrict__ buf) {
+  if (pad <= 1) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int nv = d / Vec<T>::N;
+  for (int e = blockIdx.x; e < E; e += gridDim.x) {
+    const int n = kept[e];
+    const int end = (int)min((uint64_t)((n + pad - 1) / pad) * pad, Cs);
+    for (int r = n + warp; r < end; r += nw) {
+      uint4* row = reinterpret_cast<uint4*>(buf + ((uint64_t)e * Cs + r) * d);
+      for (int v = lane; v < nv; v += 32) row[v] = make_uint4(0, 0, 0, 0);
+    }
+  }
+}
+
 template <typename T>
 __global__ void dispatch_kernel(uint64_t T_, int d, int E, int k, uint64_t Cs, uint64_t C,
                                 const T* __restrict__ x, const int32_t* __restrict__ expert,
                                 const int32_t* __restrict__ position, T* __restrict__ buf,
-                                int32_t* __restrict__ slot) {
+                                int32_t* __restrict__ slot, uint32_t pad,
+                                const int32_t* __restrict__ kept) {
+  zero_pad_rows(d, E, Cs, pad, kept, buf);
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T_;
@@ -464,7 +484,9 @@ template <typename T>
 __global__ void combine_bwd_kernel(uint64_t T_, int d, int k, const T* __restrict__ dy,
                                    const T* __restrict__ Y, const int32_t* __restrict__ slot,
                                    const float* __restrict__ gate, T* __restrict__ dY,
-                                   float* __restrict__ dgate) {
+                                   float* __restrict__ dgate, int E, uint64_t Cs, uint32_t pad,
+                                   const int32_t* __restrict__ kept) {
+  zero_pad_rows(d, E, Cs, pad, kept, dY);
   const int lane = threadIdx.x & 31;
   const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= T_) return;
@@ -709,14 +731,14 @@ void dispatch_tokens(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C,
   if (T) {
     if (dt == MOE_DTYPE_BF16)
       dispatch_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
-          T, d, E, k, Cs, C, (const __nv_bfloat16*)x, expert, position, (__nv_bfloat16*)buf, slot);
+          T, d, E, k, Cs, C, (const __nv_bfloat16*)x, expert, position, (__nv_bfloat16*)buf, slot,
+          pad, kept);
     else
       dispatch_kernel<float><<<blocks, 256, 0, st>>>(T, d, E, k, Cs, C, (const float*)x, expert,
-                                                     position, (float*)buf, slot);
+                                                     position, (float*)buf, slot, pad, kept);
     MOE_LAUNCH_CHECK("dispatch_kernel");
     count_launch();
-  }
-  if (pad > 1) {
+  } else if (pad > 1) {
     if (dt == MOE_DTYPE_BF16)
       zero_pad_kernel<__nv_bfloat16><<<E, 256, 0, st>>>(d, Cs, pad, kept, (__nv_bfloat16*)buf);
     else
@@ -749,15 +771,14 @@ void combine_backward(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C
     if (dt == MOE_DTYPE_BF16)
       combine_bwd_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
           T, d, k, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)Y, slot, gate,
-          (__nv_bfloat16*)dY, dgate);
+          (__nv_bfloat16*)dY, dgate, (int)E, Cs, pad, kept);
     else
       combine_bwd_kernel<float><<<blocks, 256, 0, st>>>(T, d, k, (const float*)dy,
                                                         (const float*)Y, slot, gate, (float*)dY,
-                                                        dgate);
+                                                        dgate, (int)E, Cs, pad, kept);
     MOE_LAUNCH_CHECK("combine_bwd_kernel");
     count_launch();
-  }
-  if (pad > 1) {
+  } else if (pad > 1) {
     if (dt == MOE_DTYPE_BF16)
       zero_pad_kernel<__nv_bfloat16><<<E, 256, 0, st>>>(d, Cs, pad, kept, (__nv_bfloat16*)dY);
     else
