@@ -440,26 +440,37 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t aph[2] = {0, 0};
     uint32_t tcount = 0;
     const uint32_t tempty0 = smem_u32(&tempty[0]);
-    for (int w = unit; w < total_work; w += nunits, ++tcount) {
-      int g, mb, nb;
-      decode(w, g, mb, nb);
-      const bool tail = is_tail(g, mb);
-      // first tile row / column of this warp, TMEM column offset, chunk count
-      const int row0 = tail ? mb * TM + (int)crank * 64 + (q & 1) * 32
-                            : mb * TM + (int)crank * BM + q * 32;
-      const int tcol = tail ? half * (BN / 4) : half * HALF;
-      const int nch = (tail ? BN / 4 : HALF) / CW;
-      int nvalid, bidx;
+    // this warp's slice of tile w: first row, output row, valid rows, columns
+    struct Geo {
+      int g, mb, nb, row0, tcol, nch, nvalid, bidx, col_base;
+      bool tail;
       long long orow0;
+    };
+    auto geo_of = [&](int w) {
+      Geo t;
+      decode(w, t.g, t.mb, t.nb);
+      t.tail = is_tail(t.g, t.mb);
+      t.row0 = t.tail ? t.mb * TM + (int)crank * 64 + (q & 1) * 32
+                      : t.mb * TM + (int)crank * BM + q * 32;
+      t.tcol = t.tail ? half * (BN / 4) : half * HALF;
+      t.nch = (t.tail ? BN / 4 : HALF) / CW;
       if (KIND == 0) {
-        nvalid = min(32, max(0, args.gm[g] - row0));
-        orow0 = (long long)args.gc[g] + row0;
-        bidx = args.gb[g];
+        t.nvalid = min(32, max(0, args.gm[t.g] - t.row0));
+        t.orow0 = (long long)args.gc[t.g] + t.row0;
+        t.bidx = args.gb[t.g];
       } else {
-        nvalid = 32;
-        bidx = args.gb[tab[g]];
-        orow0 = (long long)bidx * args.M + row0;
+        t.nvalid = 32;
+        t.bidx = args.gb[tab[t.g]];
+        t.orow0 = (long long)t.bidx * args.M + t.row0;
       }
+      t.col_base = t.nb * BN + (t.tail ? (q >> 1) * (BN / 2) : 0) + t.tcol;
+      return t;
+    };
+    for (int w = unit; w < total_work; w += nunits, ++tcount) {
+      const Geo geo = geo_of(w);
+      const int g = geo.g;
+      const int row0 = geo.row0, nch = geo.nch, nvalid = geo.nvalid, bidx = geo.bidx, tcol = geo.tcol;
+      const long long orow0 = geo.orow0;
       // REMOTE: lane s holds the exclusive row offset of source s inside this
       // expert's contiguous receive region
       int rexcl = 0, rexp = 0;
@@ -484,7 +495,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         return sidx;
       };
-      const int col_base = nb * BN + (tail ? (q >> 1) * (BN / 2) : 0) + tcol;
+      const int col_base = geo.col_base;
       if (EPI == MOE_EPI_DGELU && lane == 0 && col_base < args.N) {
         mbar_arrive_expect_tx(&ab[0], STG);
         tma_load_2d(auxb, &tmAux, &ab[0], col_base, (int)orow0);
@@ -493,12 +504,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       // tile, overlapping the wait for the accumulator)
       float* const bsm = reinterpret_cast<float*>(smem + C_::BIAS_OFF + ew * C_::BIAS_BYTES);
       const bool use_bias = C_::BIAS_BYTES > 0 && args.bias != nullptr;
-      if (use_bias) {
-        __syncwarp();  // the previous tile's reads are done
+      constexpr int NBV = (C_::BIAS_BYTES > 0 ? HALF : 32) / 32;  // bias values per lane
+      float bv[NBV];
+      if (use_bias) {  // loads in flight across the accumulator wait
         const float* bp = args.bias + (long long)bidx * args.N;
-        for (int i = lane; i < nch * CW; i += 32)
-          bsm[i] = (col_base + i < args.N) ? __ldg(bp + col_base + i) : 0.0f;
-        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < NBV; ++i) {
+          const int c = lane + 32 * i;
+          bv[i] = (c < nch * CW && col_base + c < args.N) ? __ldg(bp + col_base + c) : 0.0f;
+        }
       }
       int32_t gidx[2] = {-1, -1};
       if (EPI == MOE_EPI_GATHER_ADD && lane < nvalid) {
@@ -536,6 +550,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t acc = tcount & 1;
       mbar_wait(&tfull[acc], (tcount >> 1) & 1);
       tc_fence_after();
+      if (use_bias) {
+        __syncwarp();  // the previous tile's reads of the slice are done
+#pragma unroll
+        for (int i = 0; i < NBV; ++i) bsm[lane + 32 * i] = bv[i];
+        __syncwarp();
+      }
       const uint32_t t_row = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + tcol;
 #pragma unroll 1
       for (int c = 0; c < nch; ++c) {

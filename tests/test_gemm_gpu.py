@@ -151,11 +151,14 @@ def test_tc_ragged_m_dgelu_with_colsum():
     assert_close(cs, ref_cs, 1e-4)
 
 
-def test_tc_gather_add():
+@pytest.mark.parametrize("T,k", [(1000, 2), (1000, 1), (20000, 1), (20000, 2)])
+def test_tc_gather_add(T, k):
+    """gate dgrad + gather (dx = dlogits wg + sum_i dXe[slot_i]); T = 20000 gives
+    each SM pair several tiles (k = 1 prefetches the next tile's rows)."""
     torch.manual_seed(3)
-    T, N, K, k = 1000, 512, 64, 2
-    gsrc = (torch.rand(3000, N, device=dev) * 2 - 1).to(torch.bfloat16)
-    gidx = torch.randint(-1, 3000, (T, k), device=dev, dtype=torch.int32)
+    N, K = 512, 64
+    gsrc = (torch.rand(3 * T, N, device=dev) * 2 - 1).to(torch.bfloat16)
+    gidx = torch.randint(-1, 3 * T, (T, k), device=dev, dtype=torch.int32)
     got, ref, _, _ = ragged_m_case(torch.bfloat16, True, _lib.MOE_EPI_GATHER_ADD, N=N, K=K,
                                    groups=(T,), bvec=(0,), Cs=T, bias=False,
                                    gather=(gsrc, gidx, k))
