@@ -199,7 +199,7 @@ Layer::~Layer() {
     cudaFree(x_stage);
     for (int i = 0; i < 3; ++i) cudaStreamDestroy(hp_stream[i]);
     for (int bb = 0; bb < 2; ++bb)
-      for (int i = 0; i < 3; ++i) cudaEventDestroy(hp_ev[bb][i]);
+      for (int i = 0; i < 5; ++i) cudaEventDestroy(hp_ev[bb][i]);
   }
 }
 
@@ -591,45 +591,52 @@ void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, con
                             cudaStream_t st) {
   // Three-stream pipeline over double-buffered staging: H2D of step i+1 and
   // D2H of step i-1 overlap the compute of step i (PCIe is full duplex and the
-  // copy engines need no SMs).  Input and output stages are released
-  // separately: the H2D of step i+2 only waits for the compute of step i (its
-  // inputs consumed), the compute of step i+2 for the D2H of step i, so in
-  // steady state each copy engine streams back to back and the step time is
-  // max(H2D, compute, D2H).  The caller's stream waits for this step's D2H, so
-  // y_host / dx_host / the gradients are valid once `st` reaches this call.
+  // copy engines need no SMs).  Finer-grained than whole steps: the forward
+  // starts once x has landed (dy still in flight), y goes back to the host
+  // while the backward runs, and input / output stages are released
+  // separately (the H2D of step i+2 only waits for the compute of step i, the
+  // forward of step i+2 for the D2H of step i), so in steady state each copy
+  // engine streams back to back and the step time is max(H2D, compute, D2H).
+  // The caller's stream waits for this step's D2H, so y_host / dx_host / the
+  // gradients are valid once `st` reaches this call.
   const uint64_t bytes = T * dm * esz;
   if (!x_stage) {
     MOE_CUDA(cudaMalloc(&x_stage, 8 * bytes + 64));
     for (int i = 0; i < 3; ++i) MOE_CUDA(cudaStreamCreateWithFlags(&hp_stream[i], cudaStreamNonBlocking));
     for (int b = 0; b < 2; ++b)
-      for (int i = 0; i < 3; ++i)
+      for (int i = 0; i < 5; ++i)
         MOE_CUDA(cudaEventCreateWithFlags(&hp_ev[b][i], cudaEventDisableTiming));
     // the first step's copies must not start before work already queued on st
-    MOE_CUDA(cudaEventRecord(hp_ev[0][2], st));
-    MOE_CUDA(cudaStreamWaitEvent(hp_stream[0], hp_ev[0][2], 0));
-    MOE_CUDA(cudaStreamWaitEvent(hp_stream[1], hp_ev[0][2], 0));
+    MOE_CUDA(cudaEventRecord(hp_ev[0][4], st));
+    MOE_CUDA(cudaStreamWaitEvent(hp_stream[0], hp_ev[0][4], 0));
+    MOE_CUDA(cudaStreamWaitEvent(hp_stream[1], hp_ev[0][4], 0));
   }
   cudaStream_t h2d = hp_stream[0], comp = hp_stream[1], d2h = hp_stream[2];
   const int b = (int)(hp_iter & 1);
+  cudaEvent_t* ev_b = hp_ev[b];
   uint8_t* base = static_cast<uint8_t*>(x_stage) + (uint64_t)b * 4 * bytes;
   void* xd = base;
   void* dyd = base + bytes;
   void* yd = base + 2 * bytes;
   void* dxd = base + 3 * bytes;
-  if (hp_iter >= 2) MOE_CUDA(cudaStreamWaitEvent(h2d, hp_ev[b][1], 0));  // inputs b consumed
+  if (hp_iter >= 2) MOE_CUDA(cudaStreamWaitEvent(h2d, ev_b[3], 0));  // inputs b consumed
   MOE_CUDA(cudaMemcpyAsync(xd, x_host, bytes, cudaMemcpyHostToDevice, h2d));
+  MOE_CUDA(cudaEventRecord(ev_b[0], h2d));
   MOE_CUDA(cudaMemcpyAsync(dyd, dy_host, bytes, cudaMemcpyHostToDevice, h2d));
-  MOE_CUDA(cudaEventRecord(hp_ev[b][0], h2d));
-  MOE_CUDA(cudaStreamWaitEvent(comp, hp_ev[b][0], 0));
-  if (hp_iter >= 2) MOE_CUDA(cudaStreamWaitEvent(comp, hp_ev[b][2], 0));  // outputs b drained
+  MOE_CUDA(cudaEventRecord(ev_b[1], h2d));
+  MOE_CUDA(cudaStreamWaitEvent(comp, ev_b[0], 0));
+  if (hp_iter >= 2) MOE_CUDA(cudaStreamWaitEvent(comp, ev_b[4], 0));  // outputs b drained
   forward(w, xd, yd, nullptr, nullptr, nullptr, comp);
+  MOE_CUDA(cudaEventRecord(ev_b[2], comp));
+  MOE_CUDA(cudaStreamWaitEvent(comp, ev_b[1], 0));
   backward(w, dyd, d_aux, dxd, g, comp);
-  MOE_CUDA(cudaEventRecord(hp_ev[b][1], comp));
-  MOE_CUDA(cudaStreamWaitEvent(d2h, hp_ev[b][1], 0));
+  MOE_CUDA(cudaEventRecord(ev_b[3], comp));
+  MOE_CUDA(cudaStreamWaitEvent(d2h, ev_b[2], 0));
   MOE_CUDA(cudaMemcpyAsync(y_host, yd, bytes, cudaMemcpyDeviceToHost, d2h));
+  MOE_CUDA(cudaStreamWaitEvent(d2h, ev_b[3], 0));
   MOE_CUDA(cudaMemcpyAsync(dx_host, dxd, bytes, cudaMemcpyDeviceToHost, d2h));
-  MOE_CUDA(cudaEventRecord(hp_ev[b][2], d2h));
-  MOE_CUDA(cudaStreamWaitEvent(st, hp_ev[b][2], 0));
+  MOE_CUDA(cudaEventRecord(ev_b[4], d2h));
+  MOE_CUDA(cudaStreamWaitEvent(st, ev_b[4], 0));
   ++hp_iter;
 }
 

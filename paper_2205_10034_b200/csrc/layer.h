@@ -74,7 +74,8 @@ struct Layer {
   const void* x_saved_ptr = nullptr;
   void* x_stage = nullptr;          // host-buffer pipeline: 2 x (x, dy, y, dx)
   cudaStream_t hp_stream[3] = {};   // h2d, compute, d2h
-  cudaEvent_t hp_ev[2][3] = {};     // per stage: h2d done, compute done, d2h done
+  // per stage: x landed, dy landed, forward done, backward done, d2h done
+  cudaEvent_t hp_ev[2][5] = {};
   uint64_t hp_iter = 0;
   bool has_forward = false;
   // backward: weight-gradient GEMMs on a side stream next to the data-gradient
