@@ -52,7 +52,7 @@ def peaks():
     if os.path.exists(path):
         with open(path) as f:
             m = json.load(f)
-        for key in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained"):
+        for key in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained", "sm_max_mhz"):
             if key in m:
                 p[key] = float(m[key])
         p["source"] = "measured (MEASURED_PEAKS.json)"
@@ -350,10 +350,18 @@ def main():
     if os.path.exists(prof_path):
         with open(prof_path) as f:
             traffic = json.load(f).get(args.config, {}).get("dram_bytes_per_launch")
-    roof = {"kernel": "tc_gemm_kernel (6 expert GEMMs/step: ffn1, ffn2, 2x dgrad, 2x wgrad)",
-            "bound": "tensor", "achieved": achieved_tf, "peak": pk["bf16_tflops_sustained"],
-            "unit": "TFLOP/s", "frac": (achieved_tf / pk["bf16_tflops_sustained"]) if achieved_tf else None,
-            "traffic": traffic, "peak_source": pk["source"] + ", sustained",
+    if dtype == torch.bfloat16:
+        kname, bound, peak = ("tc_gemm_kernel (6 expert GEMMs/step: ffn1, ffn2, 2x dgrad, 2x wgrad)",
+                              "tensor", pk["bf16_tflops_sustained"])
+        psrc = pk["source"] + ", sustained"
+    else:  # c1: fp32 SIMT GEMMs (TF32 would break the 1e-5 tolerance)
+        props = torch.cuda.get_device_properties(dev)
+        peak = props.multi_processor_count * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+        kname, bound = "simt_gemm_kernel (6 expert GEMMs/step, fp32 FFMA)", "fp32"
+        psrc = "nominal FP32 FFMA: SMs x 128 lanes x 2 x max SM clock"
+    roof = {"kernel": kname, "bound": bound, "achieved": achieved_tf, "peak": peak,
+            "unit": "TFLOP/s", "frac": (achieved_tf / peak) if achieved_tf else None,
+            "traffic": traffic, "peak_source": psrc,
             "flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
             "gemm_share_of_step": gemm_ms / ms_step if ms_step else None}
 
