@@ -19,6 +19,7 @@
 // prefetch_cache.cpp:86-95, ring_offload.hpp:21); DESIGN.md §K5.
 #include <cuda.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -817,10 +818,14 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   using C_ = Cfg<BN, EPI, CF32, CG>;
   constexpr int BH = BN / CG;
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN, KIND, EPI, CF32, CG, REMOTE>;
-  static bool attr = false;
-  if (!attr) {
+  // the smem opt-in is per device: remember which devices were configured
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  MOE_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
     MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
-    attr = true;
+    configured.fetch_or(bit, std::memory_order_acq_rel);
   }
   CUtensorMap ta, tb, tcm, tc2, tax;
   if (KIND == 0) {
@@ -869,7 +874,7 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   a.ldc = (long long)p.ldc;
   a.transpose_c = p.transpose_c;
   a.num_b = (int)p.num_b;
-  static RemoteOut ro;  // host staging of the remote descriptor (copied into the launch)
+  RemoteOut ro;  // remote descriptor (copied into the launch parameters)
   std::memset(&ro, 0, sizeof(ro));
   if (REMOTE) {
     require(remote != nullptr && remote->P <= 8, MOE_ERR_LOGIC, "gemm: remote rows descriptor");
