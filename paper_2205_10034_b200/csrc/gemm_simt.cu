@@ -10,7 +10,13 @@
 namespace moe {
 namespace simt {
 
-constexpr int BM = 64, BN = 64, BK = 16, THREADS = 256, MAX_GROUPS = 1024;
+// 128 x 128 tiles, 16-deep K slices, 256 threads each owning an 8 x 8 block
+// of C (rows ty*4 + {0..3} and 64 + ty*4 + {0..3}, same for columns with tx):
+// conflict-free 16-byte shared loads, packed FFMA2 (two fp32 FMAs per
+// instruction, exact fp32 rounding), next K slice prefetched into registers
+// while the current one is multiplied.
+constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256, MAX_GROUPS = 1024;
+constexpr int PAD = 4;
 
 struct Args {
   int kind, epi, groups, M, N, K, b_mn, transpose_c;
@@ -27,9 +33,14 @@ struct Args {
   int gk;
 };
 
-__global__ void __launch_bounds__(THREADS) simt_gemm_kernel(const Args a) {
-  __shared__ float As[BK][BM + 4];
-  __shared__ float Bs[BK][BN + 4];
+// One K slice of the A / B tile in registers: 2 float4 per thread each.
+struct Slice {
+  float4 a[2], b[2];
+};
+
+__global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
+  __shared__ __align__(16) float As[2][BK][BM + PAD];
+  __shared__ __align__(16) float Bs[2][BK][BN + PAD];
   __shared__ int tab[MAX_GROUPS + 1];
   __shared__ int cnt[MAX_GROUPS];
   const int tid = threadIdx.x;
@@ -61,6 +72,9 @@ __global__ void __launch_bounds__(THREADS) simt_gemm_kernel(const Args a) {
   }
   __syncthreads();
   const int total = a.kind == 0 ? tab[G] : cnt[0] * nbm_k * nbn;
+  // vector (16-byte) global loads need 4-element aligned rows
+  const bool a_vec = (a.lda % 4) == 0 && (reinterpret_cast<uintptr_t>(a.A) & 15) == 0;
+  const bool b_vec = (a.ldb % 4) == 0 && (reinterpret_cast<uintptr_t>(a.B) & 15) == 0;
 
   const int tx = tid % 16, ty = tid / 16;
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -81,7 +95,11 @@ __global__ void __launch_bounds__(THREADS) simt_gemm_kernel(const Args a) {
       mb = (w % per) / nbn;
       nb = (w % per) % nbn;
     }
-    float acc[4][4] = {};
+    float2 acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
     // K iteration: RAGGED_M -> one range [0,K) on row base ga[g]+mb*BM;
     // RAGGED_K -> rows of every group of segment g.
     const int q0 = a.kind == 0 ? g : tab[g];
@@ -90,61 +108,122 @@ __global__ void __launch_bounds__(THREADS) simt_gemm_kernel(const Args a) {
       const int klen = a.kind == 0 ? a.K : a.gm[q];
       const int mrows = a.kind == 0 ? a.gm[q] : a.M;
       const long long r0 = a.ga[q];
-      for (int k0 = 0; k0 < klen; k0 += BK) {
-        for (int i = tid; i < BM * BK; i += THREADS) {
-          int mm, kk;
-          float v = 0.f;
+      const long long bbase = a.kind == 0 ? (long long)a.gb[q] * (a.b_mn ? a.K : a.N) : r0;
+      // element (m, k) of A / (n, k) of B with bounds (0 outside)
+      auto ldA = [&](int m, int k) -> float {
+        if (m >= mrows || k >= klen) return 0.f;
+        return a.kind == 0 ? a.A[(r0 + m) * a.lda + k] : a.A[(r0 + k) * a.lda + m];
+      };
+      auto ldB = [&](int n, int k) -> float {
+        if (n >= a.N || k >= klen) return 0.f;
+        if (a.kind == 0 && !a.b_mn) {
+          const long long br = bbase + n;
+          return br < a.b_rows ? a.B[br * a.ldb + k] : 0.f;
+        }
+        if (a.kind == 0) {
+          const long long br = bbase + k;
+          return br < a.b_rows ? a.B[br * a.ldb + n] : 0.f;
+        }
+        return a.B[(bbase + k) * a.ldb + n];
+      };
+      // thread -> float4 of the slice: "contiguous-K" layouts (A of RAGGED_M,
+      // B K-major) take 4 k of one row; "contiguous-M/N" layouts take 4 rows
+      // of one k.  Index f = tid + 256 i, i = 0, 1.
+      auto fetch = [&](int k0, Slice& sl) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int f = tid + THREADS * i;
+          if (a.kind == 0) {  // A: [m][k]
+            const int mm = f >> 2, k = k0 + (f & 3) * 4, m = mb * BM + mm;
+            if (a_vec && m < mrows && k + 3 < klen)
+              sl.a[i] = __ldg(reinterpret_cast<const float4*>(a.A + (r0 + m) * a.lda + k));
+            else
+              sl.a[i] = make_float4(ldA(m, k), ldA(m, k + 1), ldA(m, k + 2), ldA(m, k + 3));
+          } else {  // A: [k][m]
+            const int kk = f >> 5, m = mb * BM + (f & 31) * 4, k = k0 + kk;
+            if (a_vec && m + 3 < mrows && k < klen)
+              sl.a[i] = __ldg(reinterpret_cast<const float4*>(a.A + (r0 + k) * a.lda + m));
+            else
+              sl.a[i] = make_float4(ldA(m, k), ldA(m + 1, k), ldA(m + 2, k), ldA(m + 3, k));
+          }
+          if (a.kind == 0 && !a.b_mn) {  // B: [n][k]
+            const int nn = f >> 2, k = k0 + (f & 3) * 4, n = nb * BN + nn;
+            const long long br = bbase + n;
+            if (b_vec && n < a.N && k + 3 < klen && br < a.b_rows)
+              sl.b[i] = __ldg(reinterpret_cast<const float4*>(a.B + br * a.ldb + k));
+            else
+              sl.b[i] = make_float4(ldB(n, k), ldB(n, k + 1), ldB(n, k + 2), ldB(n, k + 3));
+          } else {  // B: [k][n]
+            const int kk = f >> 5, n = nb * BN + (f & 31) * 4, k = k0 + kk;
+            const long long br = bbase + k;
+            if (b_vec && n + 3 < a.N && k < klen && (a.kind != 0 || br < a.b_rows))
+              sl.b[i] = __ldg(reinterpret_cast<const float4*>(a.B + br * a.ldb + n));
+            else
+              sl.b[i] = make_float4(ldB(n, k), ldB(n + 1, k), ldB(n + 2, k), ldB(n + 3, k));
+          }
+        }
+      };
+      auto stash = [&](int buf, const Slice& sl) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int f = tid + THREADS * i;
           if (a.kind == 0) {
-            mm = i / BK; kk = i % BK;
-            const int m = mb * BM + mm, k = k0 + kk;
-            if (m < mrows && k < klen) v = a.A[(r0 + m) * a.lda + k];
+            const int mm = f >> 2, kq = (f & 3) * 4;
+            As[buf][kq][mm] = sl.a[i].x;
+            As[buf][kq + 1][mm] = sl.a[i].y;
+            As[buf][kq + 2][mm] = sl.a[i].z;
+            As[buf][kq + 3][mm] = sl.a[i].w;
           } else {
-            kk = i / BM; mm = i % BM;
-            const int m = mb * BM + mm, k = k0 + kk;
-            if (m < mrows && k < klen) v = a.A[(r0 + k) * a.lda + m];
+            *reinterpret_cast<float4*>(&As[buf][f >> 5][(f & 31) * 4]) = sl.a[i];
           }
-          As[kk][mm] = v;
-        }
-        for (int i = tid; i < BN * BK; i += THREADS) {
-          int nn, kk;
-          float v = 0.f;
           if (a.kind == 0 && !a.b_mn) {
-            nn = i / BK; kk = i % BK;
-            const int n = nb * BN + nn, k = k0 + kk;
-            const long long br = (long long)a.gb[q] * a.N + n;
-            if (n < a.N && k < klen && br < a.b_rows) v = a.B[br * a.ldb + k];
-          } else if (a.kind == 0) {
-            kk = i / BN; nn = i % BN;
-            const int n = nb * BN + nn, k = k0 + kk;
-            const long long br = (long long)a.gb[q] * a.K + k;
-            if (n < a.N && k < klen && br < a.b_rows) v = a.B[br * a.ldb + n];
+            const int nn = f >> 2, kq = (f & 3) * 4;
+            Bs[buf][kq][nn] = sl.b[i].x;
+            Bs[buf][kq + 1][nn] = sl.b[i].y;
+            Bs[buf][kq + 2][nn] = sl.b[i].z;
+            Bs[buf][kq + 3][nn] = sl.b[i].w;
           } else {
-            kk = i / BN; nn = i % BN;
-            const int n = nb * BN + nn, k = k0 + kk;
-            if (n < a.N && k < klen) v = a.B[(r0 + k) * a.ldb + n];
+            *reinterpret_cast<float4*>(&Bs[buf][f >> 5][(f & 31) * 4]) = sl.b[i];
           }
-          Bs[kk][nn] = v;
         }
-        __syncthreads();
+      };
+      Slice sl;
+      fetch(0, sl);
+      __syncthreads();  // previous tile's readers are done with both buffers
+      stash(0, sl);
+      __syncthreads();
+      int buf = 0;
+      for (int k0 = 0; k0 < klen; k0 += BK) {
+        const bool more = k0 + BK < klen;
+        if (more) fetch(k0 + BK, sl);  // in flight during the FMAs below
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
-          float av[4], bv[4];
+          const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+          const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+          const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+          const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+          const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+          const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
+                                make_float2(b1.x, b1.y), make_float2(b1.z, b1.w)};
 #pragma unroll
-          for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+          for (int i = 0; i < 8; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+            for (int j = 0; j < 4; ++j)
+              acc[i][j] = __ffma2_rn(make_float2(av[i], av[i]), bv[j], acc[i][j]);
         }
-        __syncthreads();
+        if (more) {
+          stash(buf ^ 1, sl);
+          __syncthreads();
+          buf ^= 1;
+        }
       }
+      __syncthreads();
     }
-    // epilogue
+    // epilogue: thread rows ty*4 + {0..3}, 64 + ty*4 + {0..3}; columns likewise
     const int bidx = a.kind == 0 ? a.gb[g] : a.gb[tab[g]];
-    for (int i = 0; i < 4; ++i) {
-      const int m = mb * BM + ty * 4 + i;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = mb * BM + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
       long long orow;
       if (a.kind == 0) {
         if (m >= a.gm[g]) continue;
@@ -153,10 +232,11 @@ __global__ void __launch_bounds__(THREADS) simt_gemm_kernel(const Args a) {
         if (m >= a.M) continue;
         orow = (long long)bidx * a.M + m;
       }
-      for (int j = 0; j < 4; ++j) {
-        const int n = nb * BN + tx * 4 + j;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int n = nb * BN + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
         if (n >= a.N) continue;
-        float v = acc[i][j];
+        float v = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
         if (a.epi == MOE_EPI_ATOMIC_ADD) {
           const long long idx = a.transpose_c ? (long long)n * a.ldc + orow : orow * a.ldc + n;
           atomicAdd(a.C + idx, v);
@@ -172,8 +252,8 @@ __global__ void __launch_bounds__(THREADS) simt_gemm_kernel(const Args a) {
           v *= a.aux[idx];
           if (a.colsum) atomicAdd(a.colsum + (long long)bidx * a.N + n, v);
         } else if (a.epi == MOE_EPI_GATHER_ADD) {
-          for (int i = 0; i < a.gk; ++i) {
-            const int s = a.gidx[orow * a.gk + i];
+          for (int r = 0; r < a.gk; ++r) {
+            const int s = a.gidx[orow * a.gk + r];
             if (s >= 0) v += a.gsrc[(long long)s * a.N + n];
           }
         }
