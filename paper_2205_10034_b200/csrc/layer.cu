@@ -20,7 +20,6 @@
 
 #include <cstdlib>
 #include <cstring>
-#include <optional>
 #include <string>
 #include <vector>
 
@@ -53,7 +52,6 @@ void* dalloc_bytes(std::vector<void*>& owned, uint64_t n) {
 }  // namespace
 
 Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
-  if (const char* v = std::getenv("MOE_OVERLAP_BWD")) overlap_bwd = std::atoi(v);
   E = d.num_experts;
   k = d.top_k;
   dm = d.d_model;
@@ -186,13 +184,6 @@ Layer::~Layer() {
     p2p_teardown(win);
   }
   for (int i = 0; i < kMaxPhases + 1; ++i) cudaEventDestroy(ev[i]);
-  if (side) {
-    cudaStreamSynchronize(side);
-    cudaStreamDestroy(side);
-    cudaEventDestroy(ev_fork);
-    cudaEventDestroy(ev_dh);
-    cudaEventDestroy(ev_join);
-  }
   for (void* p : owned) cudaFree(p);
   if (x_stage) {
     for (int i = 0; i < 3; ++i) cudaStreamSynchronize(hp_stream[i]);
@@ -434,28 +425,6 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     }
     grouped_gemm(p, s);
   };
-  // Overlap (MOE_OVERLAP_BWD=n, bf16): the fp32-output weight-gradient GEMMs
-  // run on a side stream on n SMs while the data-gradient GEMMs use the rest:
-  // wgrad_w2 || dgrad_ffn2, then wgrad_w1 || dgrad_ffn1.
-  const bool ovl = overlap_bwd > 0 && dt == MOE_DTYPE_BF16 && !profiling;
-  const int split = ovl ? std::max(2, std::min(num_sms() - 2, overlap_bwd)) & ~1 : 0;
-  std::optional<GemmCtaBudget> main_budget;
-  if (ovl) {
-    if (!side) {
-      MOE_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-      MOE_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-      MOE_CUDA(cudaEventCreateWithFlags(&ev_dh, cudaEventDisableTiming));
-      MOE_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    }
-    MOE_CUDA(cudaEventRecord(ev_fork, st));
-    MOE_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
-    {
-      GemmCtaBudget b(split);
-      wgrad(false, side);
-    }
-    group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, side, p2p ? (uint64_t)P * Cs : Cs);
-    main_budget.emplace(num_sms() - split);
-  }
   // K5^T dgrad: dH = (dY W2) * gelu'(h) (stored by ffn1), db1 = column sums
   // of dH fused into the same epilogue; dXe = dH W1
   MOE_CUDA(cudaMemsetAsync(g.db1, 0, (uint64_t)El * dff * 4, st));
@@ -474,15 +443,6 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("dgrad_ffn2", st);
-  if (ovl) {
-    MOE_CUDA(cudaEventRecord(ev_dh, st));
-    MOE_CUDA(cudaStreamWaitEvent(side, ev_dh, 0));
-    {
-      GemmCtaBudget b(split);
-      wgrad(true, side);
-    }
-    MOE_CUDA(cudaEventRecord(ev_join, side));
-  }
   const bool fused_return = p2p && dt == MOE_DTYPE_BF16;
   {
     moe_gemm_problem_t p = expert_problem();
@@ -508,15 +468,12 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   }
   else if (P > 1) a2a(dXl, dXh, El * Cs * dm * esz, st);
   mark("a2a_dx", st);
-  main_budget.reset();
-  if (!ovl) {
-    wgrad(true, st);
-    mark("wgrad_w1", st);
-    wgrad(false, st);
-    mark("wgrad_w2", st);
-    group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs);
-    mark("bias_grads", st);
-  }
+  wgrad(true, st);
+  mark("wgrad_w1", st);
+  wgrad(false, st);
+  mark("wgrad_w2", st);
+  group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs);
+  mark("bias_grads", st);
   if (p2p) p2p_wait(win, SLOT_DX, ph, st);
   // gate dgrad with the combine backward folded into its epilogue:
   // dx[t] = dlogits[t] wg + sum_i dXe[slot_i]; dwg = dlogits^T x (split-K)
@@ -582,7 +539,6 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     MOE_NCCL(ncclGroupEnd());
   }
   mark("allreduce_gate", st);
-  if (ovl) MOE_CUDA(cudaStreamWaitEvent(st, ev_join, 0));  // weight gradients done
   if (p2p) p2p_signal(win, SLOT_PHASE, ph, st);
 }
 

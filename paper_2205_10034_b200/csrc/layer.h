@@ -78,11 +78,6 @@ struct Layer {
   cudaEvent_t hp_ev[2][5] = {};
   uint64_t hp_iter = 0;
   bool has_forward = false;
-  // backward: weight-gradient GEMMs on a side stream next to the data-gradient
-  // GEMMs, each on its own share of the SMs (MOE_OVERLAP_BWD)
-  int overlap_bwd = 0;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_dh = nullptr, ev_join = nullptr;
   // profiling
   bool profiling = false;
   int nphase = 0;
