@@ -341,6 +341,42 @@ uint32_t moe_grad_buckets_count(moe_grad_buckets_t b);
 moe_status_t moe_grad_buckets_ids(moe_grad_buckets_t b, uint32_t i, uint64_t* ids,
                                   uint32_t capacity, uint32_t* n);
 
+/* Algorithm-1 CPU cache policy for sparse (expert) parameter blocks, the
+ * cache of SE-MoE's 2D prefetch.  Replaces SparseCache /
+ * CachePolicyParams (prefetch_cache.hpp:18-83) with identical decisions:
+ * resident -> CACHE_HIT (count += 1); occupancy + 1 < cpu_size -> FETCHED_FRESH
+ * (count 1); coldest count >= threshold (ties: lowest id) -> EVICTED_AND_FETCHED
+ * (victim reported); else STREAM_THROUGH.  Every decay_steps end_step() calls
+ * multiply all counts by beta.  Errors: CONFIG for beta outside (0, 1],
+ * decay_steps < 1, threshold < 0 ("cache.<field>: <reason>"). */
+typedef struct moe_cache_params {
+  uint64_t cpu_size;     /* cacheable blocks */
+  double threshold;      /* minimum hit count an eviction victim must reach */
+  double beta;           /* decay factor in (0, 1] */
+  uint32_t decay_steps;  /* steps per decay cycle, >= 1 */
+} moe_cache_params_t;
+typedef enum moe_cache_kind {
+  MOE_CACHE_HIT = 0,
+  MOE_CACHE_FETCHED_FRESH = 1,
+  MOE_CACHE_EVICTED_AND_FETCHED = 2,
+  MOE_CACHE_STREAM_THROUGH = 3
+} moe_cache_kind_t;
+typedef struct moe_cache_access {
+  int32_t kind;     /* moe_cache_kind_t */
+  uint64_t victim;  /* EVICTED_AND_FETCHED only */
+} moe_cache_access_t;
+typedef struct moe_sparse_cache* moe_sparse_cache_t;
+moe_status_t moe_sparse_cache_create(const moe_cache_params_t* params, moe_sparse_cache_t* out);
+moe_status_t moe_sparse_cache_destroy(moe_sparse_cache_t cache);
+moe_status_t moe_sparse_cache_access(moe_sparse_cache_t cache, uint64_t block,
+                                     moe_cache_access_t* out);
+moe_status_t moe_sparse_cache_end_step(moe_sparse_cache_t cache);
+/* occupancy (fresh admissions), steps into the current decay cycle, and the
+ * resident blocks with their counts sorted by id (capacity entries max) */
+moe_status_t moe_sparse_cache_state(moe_sparse_cache_t cache, uint64_t* occupancy, uint32_t* steps,
+                                    uint64_t* blocks, double* hits, uint64_t capacity,
+                                    uint64_t* resident);
+
 /* ======================================================================
  * 4. ring-of-sections inference (K7)
  * ====================================================================== */

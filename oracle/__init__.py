@@ -86,6 +86,9 @@ def ref():
             _ref.ref_splitmix64_next.argtypes = [C.POINTER(C.c_uint64)]
             _ref.ref_substream_seed.restype = C.c_uint64
             _ref.ref_substream_seed.argtypes = [C.c_uint64] * 3
+            _ref.ref_sparse_cache_run.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_uint32,
+                                                  C.c_void_p, C.c_uint64] + [C.c_void_p] * 4 + [
+                C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p]
             _ref.ref_trace_to_json.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
                                                C.c_void_p, C.c_char_p, C.c_uint64,
                                                C.POINTER(C.c_uint64)]

@@ -13,6 +13,7 @@
 #include <nlohmann/json.hpp>
 
 #include "moesim/collectives.hpp"
+#include "moesim/prefetch_cache.hpp"
 #include "moesim/ring_offload.hpp"
 #include "moesim/rng.hpp"
 #include "moesim/topology.hpp"
@@ -237,6 +238,43 @@ int ref_trace_from_json(const char* text, uint32_t* steps, uint32_t* ranks, uint
   } catch (const std::exception& e) {
     std::strncpy(err, e.what(), err_cap - 1);
     err[err_cap - 1] = 0;
+    return code_of(std::current_exception());
+  }
+}
+
+// prefetch_cache.cpp:28-64 SparseCache over an op list (ops[i] < 0: end_step,
+// else access(ops[i])); outcome kinds / victims per op (-1 for end_step) and
+// the final hits snapshot.
+int ref_sparse_cache_run(uint64_t cpu_size, double threshold, double beta, uint32_t decay_steps,
+                         const int64_t* ops, uint64_t n, int32_t* kinds, uint64_t* victims,
+                         uint64_t* snap_blocks, double* snap_hits, uint64_t snap_cap,
+                         uint64_t* snap_n, uint64_t* acc, uint32_t* steps) {
+  try {
+    SparseCache cache(CachePolicyParams{cpu_size, threshold, beta, decay_steps});
+    for (uint64_t i = 0; i < n; ++i) {
+      if (ops[i] < 0) {
+        cache.end_step();
+        kinds[i] = -1;
+        victims[i] = 0;
+        continue;
+      }
+      const AccessOutcome o = cache.access(static_cast<uint64_t>(ops[i]));
+      kinds[i] = static_cast<int32_t>(o.kind);
+      victims[i] = o.victim;
+    }
+    uint64_t k = 0;
+    for (const auto& [b, h] : cache.hits_snapshot()) {
+      if (k < snap_cap) {
+        snap_blocks[k] = b;
+        snap_hits[k] = h;
+      }
+      ++k;
+    }
+    *snap_n = k;
+    *acc = cache.acc_caches();
+    *steps = cache.steps();
+    return 0;
+  } catch (...) {
     return code_of(std::current_exception());
   }
 }

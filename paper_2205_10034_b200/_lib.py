@@ -118,6 +118,15 @@ class GemmProblem(C.Structure):
     ]
 
 
+class CacheParams(C.Structure):
+    _fields_ = [("cpu_size", C.c_uint64), ("threshold", C.c_double), ("beta", C.c_double),
+                ("decay_steps", C.c_uint32)]
+
+
+class CacheAccess(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("victim", C.c_uint64)]
+
+
 class LayerDesc(C.Structure):
     _fields_ = [
         ("num_experts", C.c_uint32),
@@ -204,6 +213,12 @@ SIGNATURES = {
     "moe_comm_create": (_I, [_VP, _U32, _U32, C.POINTER(_VP)]),
     "moe_comm_destroy": (_I, [_VP]),
     "moe_alltoall_packed": (_I, [_VP, _VP, _VP, _U64, _U32, _I, _VP]),
+    "moe_sparse_cache_create": (_I, [C.POINTER(CacheParams), C.POINTER(_VP)]),
+    "moe_sparse_cache_destroy": (_I, [_VP]),
+    "moe_sparse_cache_access": (_I, [_VP, _U64, C.POINTER(CacheAccess)]),
+    "moe_sparse_cache_end_step": (_I, [_VP]),
+    "moe_sparse_cache_state": (_I, [_VP, C.POINTER(_U64), C.POINTER(_U32), _VP, _VP, _U64,
+                                    C.POINTER(_U64)]),
     "moe_grad_buckets_create": (_I, [_VP, _U32, _VP, _VP, _VP, _U32, C.c_float, C.POINTER(_VP)]),
     "moe_grad_buckets_destroy": (_I, [_VP]),
     "moe_grad_buckets_push": (_I, [_VP, _U64, _VP, C.POINTER(C.c_int32)]),
@@ -239,6 +254,7 @@ STRUCTS = {
     "moe_gemm_problem_t": GemmProblem, "moe_layer_desc_t": LayerDesc,
     "moe_layer_params_t": LayerParams, "moe_layer_grads_t": LayerGrads,
     "moe_ring_desc_t": RingDesc, "moe_ring_timeline_t": RingTimeline,
+    "moe_cache_params_t": CacheParams, "moe_cache_access_t": CacheAccess,
 }
 for _n, _t in STRUCTS.items():  # layouts must match include/moe_b200.h exactly
     _sz = lib.moe_abi_sizeof(_n.encode())

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "buckets.h"
+#include "sparse_cache.h"
 #include "common.cuh"
 #include "kernels.h"
 #include "layer.h"
@@ -75,6 +76,8 @@ uint64_t moe_abi_sizeof(const char* n) {
   if (s == "moe_layer_grads_t") return sizeof(moe_layer_grads_t);
   if (s == "moe_ring_desc_t") return sizeof(moe_ring_desc_t);
   if (s == "moe_ring_timeline_t") return sizeof(moe_ring_timeline_t);
+  if (s == "moe_cache_params_t") return sizeof(moe_cache_params_t);
+  if (s == "moe_cache_access_t") return sizeof(moe_cache_access_t);
   return 0;
 }
 
@@ -429,6 +432,53 @@ moe_status_t moe_grad_buckets_ids(moe_grad_buckets_t b, uint32_t i, uint64_t* id
     const auto& v = g->ids(i);
     *n = (uint32_t)v.size();
     for (uint32_t q = 0; q < v.size() && q < capacity; ++q) ids[q] = v[q];
+  });
+}
+
+// ------------------------------------------------------- sparse cache -----
+moe_status_t moe_sparse_cache_create(const moe_cache_params_t* params, moe_sparse_cache_t* out) {
+  return guard([&] {
+    moe::arg_check(params != nullptr && out != nullptr, "cache: null argument");
+    *out = reinterpret_cast<moe_sparse_cache_t>(new moe::SparseCache(*params));
+  });
+}
+
+moe_status_t moe_sparse_cache_destroy(moe_sparse_cache_t cache) {
+  return guard([&] { delete reinterpret_cast<moe::SparseCache*>(cache); });
+}
+
+moe_status_t moe_sparse_cache_access(moe_sparse_cache_t cache, uint64_t block,
+                                     moe_cache_access_t* out) {
+  return guard([&] {
+    moe::arg_check(cache != nullptr && out != nullptr, "cache: null argument");
+    *out = reinterpret_cast<moe::SparseCache*>(cache)->access(block);
+  });
+}
+
+moe_status_t moe_sparse_cache_end_step(moe_sparse_cache_t cache) {
+  return guard([&] {
+    moe::arg_check(cache != nullptr, "cache: null argument");
+    reinterpret_cast<moe::SparseCache*>(cache)->end_step();
+  });
+}
+
+moe_status_t moe_sparse_cache_state(moe_sparse_cache_t cache, uint64_t* occupancy, uint32_t* steps,
+                                    uint64_t* blocks, double* hits, uint64_t capacity,
+                                    uint64_t* resident) {
+  return guard([&] {
+    auto* c = reinterpret_cast<moe::SparseCache*>(cache);
+    moe::arg_check(c != nullptr, "cache: null argument");
+    if (occupancy) *occupancy = c->occupancy();
+    if (steps) *steps = c->steps();
+    uint64_t n = 0;
+    for (const auto& [b, h] : c->counts()) {
+      if (n < capacity) {
+        if (blocks) blocks[n] = b;
+        if (hits) hits[n] = h;
+      }
+      ++n;
+    }
+    if (resident) *resident = n;
   });
 }
 

@@ -267,6 +267,57 @@ class GradBuckets:
             pass
 
 
+CACHE_HIT, FETCHED_FRESH, EVICTED_AND_FETCHED, STREAM_THROUGH = 0, 1, 2, 3
+CACHE_KIND_NAMES = ("cache_hit", "fetched_fresh", "evicted_and_fetched", "stream_through")
+
+
+class SparseCache:
+    """prefetch_cache.hpp:43-83 SparseCache over moe_sparse_cache_* (Algorithm-1
+    CPU cache policy). access(block) -> (kind, victim); kind names as
+    access_kind_name (prefetch_cache.cpp:16-24)."""
+
+    def __init__(self, cpu_size: int, threshold: float = 1.0, beta: float = 1.0,
+                 decay_steps: int = 1):
+        from ._lib import CacheParams
+        p = CacheParams(cpu_size, float(threshold), float(beta), decay_steps)
+        h = C.c_void_p()
+        call("moe_sparse_cache_create", C.byref(p), C.byref(h))
+        self._h = h
+
+    def access(self, block: int):
+        from ._lib import CacheAccess
+        out = CacheAccess()
+        call("moe_sparse_cache_access", self._h, block, C.byref(out))
+        return int(out.kind), int(out.victim)
+
+    def end_step(self) -> None:
+        call("moe_sparse_cache_end_step", self._h)
+
+    def state(self):
+        """(occupancy, steps, {block: hit count}) — hits_snapshot() is the dict."""
+        occ, st, n = C.c_uint64(0), C.c_uint32(0), C.c_uint64(0)
+        call("moe_sparse_cache_state", self._h, C.byref(occ), C.byref(st), None, None, 0, C.byref(n))
+        blocks = (C.c_uint64 * max(n.value, 1))()
+        hits = (C.c_double * max(n.value, 1))()
+        call("moe_sparse_cache_state", self._h, None, None, C.cast(blocks, C.c_void_p),
+             C.cast(hits, C.c_void_p), n.value, C.byref(n))
+        return occ.value, st.value, {int(blocks[i]): float(hits[i]) for i in range(n.value)}
+
+    def hit_count(self, block: int) -> float:
+        return self.state()[2].get(block, 0.0)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            call("moe_sparse_cache_destroy", self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 LOAD, COMPUTE, RELEASE = 0, 1, 2
 
 

@@ -140,6 +140,26 @@ def ref_trace_from_json(text):
             "counts": counts[:n].astype(np.int64).tolist()}
 
 
+def ref_sparse_cache(params, ops):
+    r = oracle.ref()
+    n = len(ops)
+    o = np.asarray(ops, dtype=np.int64)
+    kinds = np.zeros(max(n, 1), dtype=np.int32)
+    victims = np.zeros(max(n, 1), dtype=np.uint64)
+    sb = np.zeros(4096, dtype=np.uint64)
+    sh = np.zeros(4096, dtype=np.float64)
+    sn, acc, st = C.c_uint64(0), C.c_uint64(0), C.c_uint32(0)
+    rc = r.ref_sparse_cache_run(C.c_uint64(params[0]), C.c_double(params[1]), C.c_double(params[2]),
+                                C.c_uint32(params[3]), oracle.P(o), C.c_uint64(n), oracle.P(kinds),
+                                oracle.P(victims), oracle.P(sb), oracle.P(sh), C.c_uint64(4096),
+                                C.byref(sn), C.byref(acc), C.byref(st))
+    if rc:
+        return {"error": rc}
+    return {"kinds": kinds[:n].tolist(), "victims": victims[:n].astype(np.int64).tolist(),
+            "snapshot": [[int(sb[i]), float(sh[i])] for i in range(sn.value)],
+            "acc_caches": acc.value, "steps": st.value}
+
+
 def main():
     assert oracle.ref() is not None, "build the reference first: make -C oracle ref"
     gold = {"source": "oracle/_ref/libmoesim_ref.so built from /root/reference/proj (see oracle/Makefile)"}
@@ -233,6 +253,36 @@ def main():
         '{"steps":1,"ranks":1,"experts":2,"tokens_per_rank":2,"counts":[[[2,0]]],"schema_version":1}',
     ]
     gold["trace_from_json"] = [{"json": t, "expected": ref_trace_from_json(t)} for t in bad]
+
+    # prefetch_cache.cpp:28-64 — test_prefetch_cache.cpp:77-193 cases + random sweeps
+    sc = [
+        {"params": [4, 1.0, 1.0, 1], "ops": [100]},
+        {"params": [4, 1.0, 1.0, 1], "ops": [100, 100]},
+        {"params": [3, 1.0, 1.0, 1], "ops": [1, 1, 1, 2, 3]},
+        {"params": [3, 5.0, 1.0, 1], "ops": [1, 1, 1, 2, 3]},
+        {"params": [0, 1.0, 1.0, 1], "ops": [i % 3 for i in range(10)]},
+        {"params": [1, 1.0, 1.0, 1], "ops": [i % 3 for i in range(10)]},
+        {"params": [4, 1.0, 0.5, 2], "ops": [7, 7, 7, 7, -1, -1]},
+        {"params": [4, 1.0, 0.25, 3], "ops": [7, -1]},
+        {"params": [2, 0.0, 1.0, 1], "ops": [5, 3, 3, 9, 5]},          # tie-breaking / threshold 0
+    ]
+    g = sm64(4242)
+    for _ in range(40):
+        cpu = next(g) % 9
+        thr = float(next(g) % 6)
+        beta = 1.0 if next(g) % 2 == 0 else 0.5 + 0.0625 * (next(g) % 8)
+        k = (1, 2, 5)[next(g) % 3]
+        uni = 1 + next(g) % 12
+        ops = []
+        for _ in range(200):
+            ops.append(-1 if next(g) % 8 == 0 else int(next(g) % uni))
+        sc.append({"params": [cpu, thr, beta, k], "ops": ops})
+    sc.append({"params": [4, 1.0, 0.0, 1], "ops": [1]})   # beta 0 -> ConfigError
+    sc.append({"params": [4, 1.0, 1.0, 0], "ops": [1]})   # decay_steps 0 -> ConfigError
+    sc.append({"params": [4, -1.0, 1.0, 1], "ops": [1]})  # threshold < 0 -> ConfigError
+    for ent in sc:
+        ent["expected"] = ref_sparse_cache(ent["params"], ent["ops"])
+    gold["sparse_cache"] = sc
 
     with open(os.path.join(OUT, "reference_golden.json"), "w") as f:
         json.dump(gold, f, indent=1, sort_keys=True)
