@@ -12,10 +12,12 @@
 //   collectives.hpp:78-79 fuse_slices/split_blob moesim::fuse_slices / split_blob
 //   workload.hpp:41-46   gen_trace/imbalance     moesim::gen_trace / imbalance_ratio
 //   ring_offload.hpp:45  build_schedule          moesim::build_schedule
+//   prefetch_cache.hpp:18-83 SparseCache          moesim::SparseCache (Algorithm-1 policy)
 //   types.hpp:24-26      ConfigError             moesim::ConfigError
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <numeric>
 #include <optional>
 #include <stdexcept>
@@ -197,5 +199,78 @@ inline RingSchedule build_schedule(std::uint32_t num_layers, std::uint32_t ring_
   }
   return s;
 }
+
+// prefetch_cache.hpp:18-83: CachePolicyParams / AccessKind / AccessOutcome /
+// SparseCache with the reference's member names; decisions come from
+// moe_sparse_cache_* (identical to the reference's, tests/golden).
+struct CachePolicyParams {
+  std::size_t cpu_size = 0;
+  double threshold = 1.0;
+  double beta = 1.0;
+  std::uint32_t decay_steps = 1;
+};
+
+enum class AccessKind : std::uint8_t {
+  kCacheHit = 0,
+  kFetchedFresh,
+  kEvictedAndFetched,
+  kStreamThrough,
+};
+
+struct AccessOutcome {
+  AccessKind kind = AccessKind::kCacheHit;
+  std::uint64_t victim = 0;
+  friend bool operator==(const AccessOutcome&, const AccessOutcome&) = default;
+};
+
+class SparseCache {
+ public:
+  explicit SparseCache(CachePolicyParams params) : params_(params) {
+    const moe_cache_params_t p{params.cpu_size, params.threshold, params.beta, params.decay_steps};
+    detail::check(moe_sparse_cache_create(&p, &h_));
+  }
+  SparseCache(const SparseCache&) = delete;
+  SparseCache& operator=(const SparseCache&) = delete;
+  ~SparseCache() { moe_sparse_cache_destroy(h_); }
+
+  AccessOutcome access(std::uint64_t block) {
+    moe_cache_access_t o{};
+    detail::check(moe_sparse_cache_access(h_, block, &o));
+    return AccessOutcome{static_cast<AccessKind>(o.kind), o.victim};
+  }
+  void end_step() { detail::check(moe_sparse_cache_end_step(h_)); }
+
+  const CachePolicyParams& params() const { return params_; }
+  bool resident(std::uint64_t block) const { return hits_snapshot().count(block) != 0; }
+  std::size_t acc_caches() const {
+    std::uint64_t occ = 0;
+    detail::check(moe_sparse_cache_state(h_, &occ, nullptr, nullptr, nullptr, 0, nullptr));
+    return occ;
+  }
+  std::uint32_t steps() const {
+    std::uint32_t st = 0;
+    detail::check(moe_sparse_cache_state(h_, nullptr, &st, nullptr, nullptr, 0, nullptr));
+    return st;
+  }
+  double hit_count(std::uint64_t block) const {
+    const auto snap = hits_snapshot();
+    const auto it = snap.find(block);
+    return it == snap.end() ? 0.0 : it->second;
+  }
+  std::map<std::uint64_t, double> hits_snapshot() const {
+    std::uint64_t n = 0;
+    detail::check(moe_sparse_cache_state(h_, nullptr, nullptr, nullptr, nullptr, 0, &n));
+    std::vector<std::uint64_t> b(n);
+    std::vector<double> h(n);
+    detail::check(moe_sparse_cache_state(h_, nullptr, nullptr, b.data(), h.data(), n, &n));
+    std::map<std::uint64_t, double> out;
+    for (std::uint64_t i = 0; i < n; ++i) out.emplace(b[i], h[i]);
+    return out;
+  }
+
+ private:
+  CachePolicyParams params_;
+  moe_sparse_cache_t h_ = nullptr;
+};
 
 }  // namespace moesim

@@ -264,6 +264,53 @@ void layer_case() {
   check(moe_layer_destroy(L) == MOE_OK, "destroy");
 }
 
+// test_prefetch_cache.cpp:77-158 assertions against the drop-in SparseCache
+void sparse_cache_cases() {
+  using moesim::AccessKind;
+  using moesim::CachePolicyParams;
+  using moesim::SparseCache;
+  {
+    SparseCache cache(CachePolicyParams{4, 1.0, 1.0, 1});
+    check(cache.access(100).kind == AccessKind::kFetchedFresh, "fresh admission");
+    check(cache.hit_count(100) == 1.0 && cache.acc_caches() == 1, "fresh count");
+    check(cache.access(100).kind == AccessKind::kCacheHit && cache.hit_count(100) == 2.0, "hit");
+  }
+  {
+    SparseCache cache(CachePolicyParams{3, 1.0, 1.0, 1});
+    for (int b : {1, 1, 1, 2}) cache.access(b);
+    const auto out = cache.access(3);
+    check(out.kind == AccessKind::kEvictedAndFetched && out.victim == 2, "evict coldest");
+    check(!cache.resident(2) && cache.resident(3) && cache.hit_count(3) == 1.0, "readmit");
+  }
+  {
+    SparseCache cache(CachePolicyParams{3, 5.0, 1.0, 1});
+    for (int b : {1, 1, 1, 2}) cache.access(b);
+    check(cache.access(3).kind == AccessKind::kStreamThrough && cache.hit_count(1) == 3.0,
+          "no warm-enough victim streams through");
+  }
+  for (std::size_t size : {0u, 1u}) {
+    SparseCache cache(CachePolicyParams{size, 1.0, 1.0, 1});
+    for (int i = 0; i < 10; ++i)
+      check(cache.access(i % 3).kind == AccessKind::kStreamThrough, "cpu_size 0/1 never caches");
+    check(cache.acc_caches() == 0, "no occupancy");
+  }
+  {
+    SparseCache cache(CachePolicyParams{4, 1.0, 0.5, 2});
+    for (int i = 0; i < 4; ++i) cache.access(7);
+    cache.end_step();
+    check(cache.hit_count(7) == 4.0, "no decay before K");
+    cache.end_step();
+    check(cache.hit_count(7) == 2.0 && cache.steps() == 0, "decay after K steps");
+  }
+  bool threw = false;
+  try {
+    SparseCache bad(CachePolicyParams{4, 1.0, 0.0, 1});
+  } catch (const moesim::ConfigError& e) {
+    threw = std::string(e.what()) == "cache.beta: must be in (0, 1]";
+  }
+  check(threw, "beta 0 -> ConfigError");
+}
+
 }  // namespace
 
 int main() {
@@ -273,6 +320,8 @@ int main() {
       {"gen_trace = independent sampler, conservation, imbalance (workload.cpp:19-66)",
        workload_cases},
       {"build_schedule shapes, chains, clamping (ring_offload.cpp:31-50)", ring_cases},
+      {"SparseCache branches, eviction, decay, errors (prefetch_cache.cpp:28-64)",
+       sparse_cache_cases},
       {"MoE layer fwd+bwd from C++ through the C-ABI", layer_case},
   };
   int failed = 0;
