@@ -377,6 +377,46 @@ moe_status_t moe_sparse_cache_state(moe_sparse_cache_t cache, uint64_t* occupanc
                                     uint64_t* blocks, double* hits, uint64_t capacity,
                                     uint64_t* resident);
 
+/* 2D prefetch executed on the GPU box (the reference
+ * simulates it in run_2d_schedule, prefetch_cache.hpp:85-130): a stack of
+ * num_layers MoE layers whose expert sections live in three tiers — a
+ * backing-store file (the SSD tier, written from host_sections at create),
+ * pinned CPU blocks managed by the Algorithm-1 cache, and lookahead + 1 HBM
+ * slots.  For every (step, layer) the cache decides the backing-store I/O, the
+ * section's H2D is issued when compute(t - lookahead) starts, and compute(t)
+ * (layer forward + residual, gate weights resident) waits for it. */
+typedef struct moe_prefetch_desc {
+  uint32_t num_layers;
+  uint32_t lookahead;                 /* layers of prefetch depth, >= 1 */
+  moe_cache_params_t cache;           /* cpu_size in sections */
+  uint32_t flush_period;              /* steps between CPU->store flushes; 0 = decay_steps */
+  const void* const* host_sections;   /* [num_layers] section images (moe_ring_pack_section) */
+  const void* const* gate_weights;    /* [num_layers] device pointers (wg) */
+  const char* backing_path;           /* file for the backing store (created, removed at destroy) */
+} moe_prefetch_desc_t;
+typedef struct moe_prefetch_record {  /* one (step, layer) */
+  uint32_t step, layer;
+  int32_t kind;                       /* moe_cache_kind_t of the access */
+  uint64_t victim;
+  float io_ms;                        /* host time in backing-store reads / writes */
+  float h2d_start, h2d_end;           /* ms from the run start (CUDA events) */
+  float compute_start, compute_end;
+} moe_prefetch_record_t;
+typedef struct moe_prefetch_summary {
+  float makespan_ms, compute_total_ms, stall_total_ms, io_total_ms;
+  uint64_t bytes_read, bytes_written, h2d_bytes, section_bytes;
+  uint32_t gpu_slots;
+} moe_prefetch_summary_t;
+typedef struct moe_prefetch* moe_prefetch_t;
+moe_status_t moe_prefetch_create(moe_layer_t layer, const moe_prefetch_desc_t* desc,
+                                 moe_prefetch_t* out);
+moe_status_t moe_prefetch_destroy(moe_prefetch_t p);
+/* `steps` passes over the stack from x (device) to y; records: steps*num_layers
+ * entries or NULL.  Synchronises the stream (the timeline is read back). */
+moe_status_t moe_prefetch_run(moe_prefetch_t p, uint32_t steps, const void* x, void* y,
+                              moe_prefetch_record_t* records, moe_prefetch_summary_t* summary,
+                              void* stream);
+
 /* ======================================================================
  * 4. ring-of-sections inference (K7)
  * ====================================================================== */

@@ -127,6 +127,25 @@ class CacheAccess(C.Structure):
     _fields_ = [("kind", C.c_int32), ("victim", C.c_uint64)]
 
 
+class PrefetchDesc(C.Structure):
+    _fields_ = [("num_layers", C.c_uint32), ("lookahead", C.c_uint32), ("cache", CacheParams),
+                ("flush_period", C.c_uint32), ("host_sections", C.c_void_p),
+                ("gate_weights", C.c_void_p), ("backing_path", C.c_char_p)]
+
+
+class PrefetchRecord(C.Structure):
+    _fields_ = [("step", C.c_uint32), ("layer", C.c_uint32), ("kind", C.c_int32),
+                ("victim", C.c_uint64), ("io_ms", C.c_float), ("h2d_start", C.c_float),
+                ("h2d_end", C.c_float), ("compute_start", C.c_float), ("compute_end", C.c_float)]
+
+
+class PrefetchSummary(C.Structure):
+    _fields_ = [("makespan_ms", C.c_float), ("compute_total_ms", C.c_float),
+                ("stall_total_ms", C.c_float), ("io_total_ms", C.c_float),
+                ("bytes_read", C.c_uint64), ("bytes_written", C.c_uint64),
+                ("h2d_bytes", C.c_uint64), ("section_bytes", C.c_uint64), ("gpu_slots", C.c_uint32)]
+
+
 class LayerDesc(C.Structure):
     _fields_ = [
         ("num_experts", C.c_uint32),
@@ -213,6 +232,9 @@ SIGNATURES = {
     "moe_comm_create": (_I, [_VP, _U32, _U32, C.POINTER(_VP)]),
     "moe_comm_destroy": (_I, [_VP]),
     "moe_alltoall_packed": (_I, [_VP, _VP, _VP, _U64, _U32, _I, _VP]),
+    "moe_prefetch_create": (_I, [_VP, C.POINTER(PrefetchDesc), C.POINTER(_VP)]),
+    "moe_prefetch_destroy": (_I, [_VP]),
+    "moe_prefetch_run": (_I, [_VP, _U32, _VP, _VP, _VP, C.POINTER(PrefetchSummary), _VP]),
     "moe_sparse_cache_create": (_I, [C.POINTER(CacheParams), C.POINTER(_VP)]),
     "moe_sparse_cache_destroy": (_I, [_VP]),
     "moe_sparse_cache_access": (_I, [_VP, _U64, C.POINTER(CacheAccess)]),
@@ -255,6 +277,8 @@ STRUCTS = {
     "moe_layer_params_t": LayerParams, "moe_layer_grads_t": LayerGrads,
     "moe_ring_desc_t": RingDesc, "moe_ring_timeline_t": RingTimeline,
     "moe_cache_params_t": CacheParams, "moe_cache_access_t": CacheAccess,
+    "moe_prefetch_desc_t": PrefetchDesc, "moe_prefetch_record_t": PrefetchRecord,
+    "moe_prefetch_summary_t": PrefetchSummary,
 }
 for _n, _t in STRUCTS.items():  # layouts must match include/moe_b200.h exactly
     _sz = lib.moe_abi_sizeof(_n.encode())

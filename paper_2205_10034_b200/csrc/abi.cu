@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "buckets.h"
+#include "prefetch.h"
 #include "sparse_cache.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -78,6 +79,9 @@ uint64_t moe_abi_sizeof(const char* n) {
   if (s == "moe_ring_timeline_t") return sizeof(moe_ring_timeline_t);
   if (s == "moe_cache_params_t") return sizeof(moe_cache_params_t);
   if (s == "moe_cache_access_t") return sizeof(moe_cache_access_t);
+  if (s == "moe_prefetch_desc_t") return sizeof(moe_prefetch_desc_t);
+  if (s == "moe_prefetch_record_t") return sizeof(moe_prefetch_record_t);
+  if (s == "moe_prefetch_summary_t") return sizeof(moe_prefetch_summary_t);
   return 0;
 }
 
@@ -479,6 +483,29 @@ moe_status_t moe_sparse_cache_state(moe_sparse_cache_t cache, uint64_t* occupanc
       ++n;
     }
     if (resident) *resident = n;
+  });
+}
+
+// ---------------------------------------------------------- prefetch -----
+moe_status_t moe_prefetch_create(moe_layer_t layer, const moe_prefetch_desc_t* desc,
+                                 moe_prefetch_t* out) {
+  return guard([&] {
+    moe::arg_check(layer != nullptr && desc != nullptr && out != nullptr, "prefetch: null argument");
+    *out = reinterpret_cast<moe_prefetch_t>(
+        new moe::Prefetch2D(reinterpret_cast<moe::Layer*>(layer), *desc));
+  });
+}
+
+moe_status_t moe_prefetch_destroy(moe_prefetch_t p) {
+  return guard([&] { delete reinterpret_cast<moe::Prefetch2D*>(p); });
+}
+
+moe_status_t moe_prefetch_run(moe_prefetch_t p, uint32_t steps, const void* x, void* y,
+                              moe_prefetch_record_t* records, moe_prefetch_summary_t* summary,
+                              void* stream) {
+  return guard([&] {
+    moe::arg_check(p != nullptr && x != nullptr && y != nullptr, "prefetch: null argument");
+    reinterpret_cast<moe::Prefetch2D*>(p)->run(steps, x, y, records, summary, S(stream));
   });
 }
 

@@ -32,6 +32,19 @@ __global__ void residual_add_kernel(const T* __restrict__ a, const T* __restrict
 uint64_t align256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 }  // namespace
 
+void residual_add(moe_dtype_t dt, const void* a, const void* b, void* out, uint64_t n,
+                  cudaStream_t st) {
+  const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(n, 256), 148ull * 8);
+  if (dt == MOE_DTYPE_BF16)
+    residual_add_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        (const __nv_bfloat16*)a, (const __nv_bfloat16*)b, (__nv_bfloat16*)out, n);
+  else
+    residual_add_kernel<float><<<grid, 256, 0, st>>>((const float*)a, (const float*)b,
+                                                     (float*)out, n);
+  MOE_LAUNCH_CHECK("residual_add_kernel");
+  count_launch();
+}
+
 SectionLayout section_layout(const Layer& L) {
   SectionLayout s;
   s.w1 = 0;
@@ -132,16 +145,7 @@ void Ring::run(const void* x, void* y, moe_ring_timeline_t* tl, cudaStream_t st)
       w.w2 = s + lay.w2;
       w.b2 = reinterpret_cast<const float*>(s + lay.b2);
       L->forward(w, hbuf[cur], tmp, nullptr, nullptr, nullptr, st);
-      const unsigned grid = (unsigned)std::min<uint64_t>(ceil_div(n, 256), 148ull * 8);
-      if (L->dt == MOE_DTYPE_BF16)
-        residual_add_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
-            (const __nv_bfloat16*)hbuf[cur], (const __nv_bfloat16*)tmp,
-            (__nv_bfloat16*)hbuf[cur ^ 1], n);
-      else
-        residual_add_kernel<float><<<grid, 256, 0, st>>>((const float*)hbuf[cur],
-                                                         (const float*)tmp, (float*)hbuf[cur ^ 1], n);
-      MOE_LAUNCH_CHECK("residual_add_kernel");
-      count_launch();
+      residual_add(L->dt, hbuf[cur], tmp, hbuf[cur ^ 1], n, st);
       cur ^= 1;
       MOE_CUDA(cudaEventRecord(ev_comp1[i], st));  // release(i): slot free once compute(i) ends
     }

@@ -17,6 +17,10 @@ struct SectionLayout {
 };
 SectionLayout section_layout(const Layer& L);
 
+// out = a + b elementwise (the residual of a stacked MoE layer)
+void residual_add(moe_dtype_t dt, const void* a, const void* b, void* out, uint64_t n,
+                  cudaStream_t st);
+
 // build_schedule (ring_offload.cpp:31-50): kind 0 load, 1 compute, 2 release.
 struct RingOpRec {
   int kind;
