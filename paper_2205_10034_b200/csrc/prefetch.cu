@@ -122,6 +122,9 @@ void Prefetch2D::run(uint32_t steps, const void* x, void* y, moe_prefetch_record
   const uint64_t n = L->T * L->dm;
   const uint64_t act = n * L->esz;
   const uint64_t total = (uint64_t)steps * N;
+  // the previous run ended synchronised: forget its events before destroying them
+  for (auto& [b, blk] : blocks) blk.last = nullptr;
+  stage_last[0] = stage_last[1] = nullptr;
   for (cudaEvent_t e : evs) cudaEventDestroy(e);
   evs.clear();
   std::vector<cudaEvent_t> h0(total), h1(total), c0(total), c1(total);

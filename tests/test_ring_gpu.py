@@ -72,6 +72,17 @@ def test_prefetch2d_matches_resident_and_cache_policy(tmp_path, lookahead, cpu_s
     x = layer.make_input(9)
     y, recs, sm = pf.run(x, steps)
     torch.cuda.synchronize()
+    # a second run continues the same cache (state persists across runs)
+    pol2 = SparseCache(cpu_size, threshold, 0.5, 2)
+    for t in range(steps * N):
+        pol2.access(t % N)
+        if t % N == N - 1:
+            pol2.end_step()
+    y2, recs2, _ = pf.run(x, 1)
+    torch.cuda.synchronize()
+    names2 = ("cache_hit", "fetched_fresh", "evicted_and_fetched", "stream_through")
+    for r in recs2:
+        assert r["outcome"] == names2[pol2.access(r["layer"])[0]]
     # resident reference
     ref_layer = MoELayer(cfg)
     ref_layer.init_params(0)
