@@ -364,6 +364,14 @@ def main():
             "traffic": traffic, "peak_source": psrc,
             "flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
             "gemm_share_of_step": gemm_ms / ms_step if ms_step else None}
+    # per-GEMM view: each of the six carries 2 * rows * d * d_ff flops
+    per = []
+    for name in ("ffn1", "ffn2", "dgrad_ffn2", "dgrad_ffn1", "wgrad_w1", "wgrad_w2"):
+        ms_k = sum(v for n, v in phase_tot.items() if n.split(".", 1)[-1] == name) / args.steps
+        if ms_k > 0:
+            tf = 2.0 * rows_local * d * dff / (ms_k / 1000.0) / 1e12
+            per.append({"gemm": name, "ms": ms_k, "tflops": tf, "frac": tf / peak})
+    roof["per_gemm"] = per
 
     # ---- end to end through the host-buffer API (H2D + step + D2H) ----
     e2e = None
