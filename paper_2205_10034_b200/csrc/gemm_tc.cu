@@ -95,6 +95,7 @@ struct Args {
   long long ldc;
   int transpose_c;
   int num_b;
+  int c_direct;  // C rows not 16-byte aligned (e.g. N = E = 2): no TMA stores, scalar stores
 };
 
 // Per-peer destinations of the remote-store epilogue (RemoteRows on device).
@@ -152,11 +153,11 @@ __device__ __forceinline__ void stage_row(uint8_t* stg, uint32_t r, const float*
 // masked direct store of one row's chunk (partial tiles)
 template <bool CF32>
 __device__ __forceinline__ void store_row_direct(void* base, long long off, int ncols,
-                                                 const float* f) {
+                                                 const float* f, bool vec_ok = true) {
   constexpr int CW = CF32 ? 16 : 32;
   if (CF32) {
     float* p = reinterpret_cast<float*>(base) + off;
-    if (ncols >= CW) {
+    if (vec_ok && ncols >= CW) {
 #pragma unroll
       for (int q = 0; q < 4; ++q)
         *reinterpret_cast<float4*>(p + q * 4) =
@@ -168,7 +169,7 @@ __device__ __forceinline__ void store_row_direct(void* base, long long off, int 
     }
   } else {
     __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(base) + off;
-    if (ncols >= CW) {
+    if (vec_ok && ncols >= CW) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint4 o;
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         uint8_t* const stg = stg_base + (C_::NBUF == 2 ? (nst & 1) : 0) * STG;
         uint8_t* const stg2 = stg_base + (C_::NBUF + (C_::NBUF == 2 ? (nst & 1) : 0)) * STG;
         const int ncols = min(CW, args.N - n0);
-        const bool full_tile = nvalid == 32 && ncols == CW;
+        const bool full_tile = nvalid == 32 && ncols == CW && !args.c_direct;
         const bool row_ok = lane < nvalid;
         if (EPI == MOE_EPI_ATOMIC_ADD) {
           if (row_ok) {
@@ -725,7 +726,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (!full_tile && row_ok) {
           const long long off = (orow0 + lane) * args.ldc + n0;
-          store_row_direct<CF32>(args.C, off, ncols, f);
+          store_row_direct<CF32>(args.C, off, ncols, f, !args.c_direct);
           if (EPI == MOE_EPI_GELU) store_row_direct<CF32>(args.C2, off, ncols, f2);
         }
         if (want_colsum && !CF32) {
@@ -848,7 +849,11 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   }
   const uint64_t c_rows = p.c_rows ? p.c_rows : (KIND == 0 ? p.a_rows : (uint64_t)p.num_b * p.M);
   tcm = tc2 = tax = ta;
-  if (EPI != MOE_EPI_ATOMIC_ADD) {
+  const uint64_t c_es = CF32 ? 4 : 2;
+  const bool c_direct = (p.ldc * c_es) % 16 != 0 || (reinterpret_cast<uintptr_t>(p.C) & 15) != 0;
+  require(!c_direct || (EPI == MOE_EPI_STORE && !REMOTE), MOE_ERR_INVALID_ARGUMENT,
+          "gemm.ldc: rows must be 16-byte aligned for this epilogue");
+  if (EPI != MOE_EPI_ATOMIC_ADD && !c_direct) {
     tcm = make_map(p.C, p.N, c_rows, p.ldc, C_::CW, 32, CF32, CU_TENSOR_MAP_SWIZZLE_64B);
     if (EPI == MOE_EPI_GELU)
       tc2 = make_map(p.C2, p.N, c_rows, p.ldc, C_::CW, 32, CF32, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -874,6 +879,7 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   a.ldc = (long long)p.ldc;
   a.transpose_c = p.transpose_c;
   a.num_b = (int)p.num_b;
+  a.c_direct = c_direct ? 1 : 0;
   RemoteOut ro;  // remote descriptor (copied into the launch parameters)
   std::memset(&ro, 0, sizeof(ro));
   if (REMOTE) {
@@ -936,7 +942,8 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st, const RemoteR
   const bool f32 = p.dtype_c == MOE_DTYPE_F32;
   if (p.kind == MOE_GEMM_RAGGED_M) {
     arg_check(p.K % BK == 0, "gemm.K: must be a multiple of 64");
-    arg_check(p.N % 8 == 0, "gemm.N: must be a multiple of 8");
+    arg_check(p.N % 8 == 0 || p.epilogue == MOE_EPI_STORE,
+              "gemm.N: must be a multiple of 8 (any N for STORE)");
     arg_check(!p.transpose_c, "gemm.transpose_c: only for RAGGED_K atomic");
     const bool bmn = p.b_mn_major != 0;
     if (p.N <= 64 && !bmn && p.epilogue == MOE_EPI_STORE) {
@@ -973,7 +980,8 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st, const RemoteR
     }
   } else {
     arg_check(p.M % BM == 0, "gemm.M: RAGGED_K needs M a multiple of 128");
-    arg_check(p.N % 8 == 0, "gemm.N: must be a multiple of 8");
+    arg_check(p.N % 8 == 0 || p.epilogue == MOE_EPI_ATOMIC_ADD,
+              "gemm.N: must be a multiple of 8 (any N for ATOMIC_ADD)");
     arg_check(f32, "gemm.dtype_c: RAGGED_K writes fp32");
     if (p.epilogue == MOE_EPI_ATOMIC_ADD) {
       if (p.N <= 64) launch<64, true, true, 1, MOE_EPI_ATOMIC_ADD, true>(p, st);

@@ -214,3 +214,16 @@ def test_gradient_buckets_single_rank_scale():
     for i, g in enumerate(grads):
         assert torch.all(g == 0.25 * (i + 1))
     gb.close()
+
+
+@pytest.mark.parametrize("E,k,T,cf,dtype", [
+    (1, 1, 64, 1.0, torch.bfloat16),      # a single expert
+    (2, 2, 96, 1.0, torch.bfloat16),      # top-2 over two experts: every token uses both
+    (8, 1, 1, 1.25, torch.bfloat16),      # one token
+    (8, 2, 300, 0.05, torch.bfloat16),    # tiny capacity: most assignments dropped
+    (4, 2, 77, 2.0, torch.float32),       # fp32, ragged T
+])
+def test_layer_edge_cases(E, k, T, cf, dtype):
+    """Edge cases of Appendix A: single expert, E = k, one token, heavy drops,
+    fp32 with a ragged token count — all against the fp64 oracle."""
+    check_case(E=E, k=k, d=128, dff=256, T=T, cf=cf, dtype=dtype)
