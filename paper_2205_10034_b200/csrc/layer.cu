@@ -237,7 +237,7 @@ moe_gemm_problem_t Layer::expert_problem() const {
 
 void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const float* override_logits,
                     float* logits_out, const moe_routing_out_t* rout, cudaStream_t st) {
-  arg_check(x != nullptr && y != nullptr, "forward.x/y: must be non-null");
+  arg_check((x != nullptr && y != nullptr) || T == 0, "forward.x/y: must be non-null");
   arg_check(w.w1 && w.w2 && w.b1 && w.b2, "forward.params: expert weights must be non-null");
   arg_check(override_logits || w.wg, "forward.params.wg: gate weight required");
   nphase = 0;
@@ -366,7 +366,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
 void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, void* dx,
                      const moe_layer_grads_t& g, cudaStream_t st) {
   require(has_forward, MOE_ERR_LOGIC, "backward: no forward pass recorded on this layer");
-  arg_check(dy != nullptr && dx != nullptr, "backward.dy/dx: must be non-null");
+  arg_check((dy != nullptr && dx != nullptr) || T == 0, "backward.dy/dx: must be non-null");
   arg_check(g.dw1 && g.db1 && g.dw2 && g.db2 && g.dwg, "backward.grads: must be non-null");
   arg_check(w.wg != nullptr, "backward.params.wg: gate weight required");
   nphase = 0;

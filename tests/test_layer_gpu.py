@@ -227,3 +227,18 @@ def test_layer_edge_cases(E, k, T, cf, dtype):
     """Edge cases of Appendix A: single expert, E = k, one token, heavy drops,
     fp32 with a ragged token count — all against the fp64 oracle."""
     check_case(E=E, k=k, d=128, dff=256, T=T, cf=cf, dtype=dtype)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_layer_empty_batch(dtype):
+    """T = 0: empty outputs and exactly-zero parameter gradients."""
+    cfg = MoEConfig(8, 2, 128, 256, 1.25, 0, dtype)
+    layer = MoELayer(cfg)
+    layer.init_params(1)
+    x = torch.empty(0, 128, dtype=dtype, device="cuda")
+    y = layer.forward(x)
+    dx = layer.backward(torch.empty_like(x), d_aux=0.01)
+    torch.cuda.synchronize()
+    assert y.shape == (0, 128) and dx.shape == (0, 128)
+    for n, gr in layer.grads.items():
+        assert not gr.abs().sum().item(), n
