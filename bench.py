@@ -152,6 +152,7 @@ def run_reference_arm(args, cfg):
     if rank != 0:
         return
     import oracle
+    oracle.set_threads(len(os.sched_getaffinity(0)))  # all host cores, also under torchrun
     n = cpu_sample_tokens(cfg) // 4 if args.steps > 1 else cpu_sample_tokens(cfg)
     n = max(64, n // 64 * 64)
     for _ in range(args.warmup if args.warmup < 1 else 1):
@@ -402,6 +403,7 @@ def main():
     if rank == 0 and ws == 1 and not args.no_cpu:
         os.sched_setaffinity(0, ALL_CPUS)  # the CPU baseline gets every host core
         import oracle
+        oracle.set_threads(len(ALL_CPUS))
         n = cpu_sample_tokens(cfg)
         v, dt = cpu_oracle_tokens_per_s(cfg, n)
         cpu = {"value": v, "unit": "tokens/s", "cores": oracle.num_threads(), "kind": "port",

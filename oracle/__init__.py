@@ -73,6 +73,7 @@ def lib():
                                              + [C.c_void_p] * 13 + [C.c_double]
                                              + [C.c_void_p] * 8)
         _lib.oracle_num_threads.restype = C.c_int
+        _lib.oracle_set_threads.argtypes = [C.c_int]
     return _lib
 
 
@@ -223,6 +224,10 @@ def moe_backward(x, wg, bg, w1, b1, w2, b2, k, capacity, emulate_bf16, fwd, dy, 
 
 def num_threads() -> int:
     return int(lib().oracle_num_threads())
+
+
+def set_threads(n: int) -> None:
+    lib().oracle_set_threads(int(n))
 
 
 # ----------------------------------------------------- synthetic tensors ----
