@@ -76,6 +76,21 @@ typedef struct moe_slice_index_entry {
 moe_status_t moesim_alltoall_flat(uint64_t ranks, uint64_t n_chunks, const uint64_t* lens,
                                   const uint8_t* data, uint64_t* out_lens, uint8_t* out_data);
 
+/* collectives.cpp:31-79 alltoall_hierarchical on a (clusters, nodes_per_cluster,
+ * gpus_per_node) topology: phase 1 stages every chunk inside its source node
+ * on the GPU whose local rank matches the destination's (NVLink), phase 2
+ * moves it along the rail; delivered chunks equal moesim_alltoall_flat.  Both
+ * phases run on the GPU.  stats (NULL or 14 entries): phase-1 hops per link
+ * class [nvlink, pcie, ssd_io, tor, leaf, spin], phase-2 hops, phase-1 and
+ * phase-2 transfer counts (AlltoAllStats, collectives.hpp:38-47).  Errors as
+ * the reference: CONFIG for a zero topology dimension, INVALID_ARGUMENT for a
+ * non-square payload or a rank count that differs from the topology's. */
+moe_status_t moesim_alltoall_hierarchical(uint32_t clusters, uint32_t nodes_per_cluster,
+                                          uint32_t gpus_per_node, uint64_t ranks,
+                                          uint64_t n_chunks, const uint64_t* lens,
+                                          const uint8_t* data, uint64_t* out_lens,
+                                          uint8_t* out_data, uint64_t* stats);
+
 /* moesim::fuse_slices (collectives.hpp:78, collectives.cpp:88-98). n == 0 ->
  * INVALID_ARGUMENT ("fuse_slices: empty slice list"). blob gets sum(lens). */
 moe_status_t moesim_fuse_slices(uint64_t n, const uint64_t* lens, const uint8_t* data,

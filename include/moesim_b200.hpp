@@ -9,6 +9,8 @@
 //
 //   reference                                   here
 //   collectives.hpp:36   alltoall_flat          moesim::alltoall_flat
+//   collectives.hpp:54-55 alltoall_hierarchical  moesim::alltoall_hierarchical (+ AlltoAllStats)
+//   topology.hpp:15-60   LinkClass/GpuId/Topology moesim::Topology (shape, route; no timing)
 //   collectives.hpp:78-79 fuse_slices/split_blob moesim::fuse_slices / split_blob
 //   workload.hpp:41-46   gen_trace/imbalance     moesim::gen_trace / imbalance_ratio
 //   ring_offload.hpp:45  build_schedule          moesim::build_schedule
@@ -16,6 +18,7 @@
 //   types.hpp:24-26      ConfigError             moesim::ConfigError
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <map>
 #include <numeric>
@@ -76,6 +79,116 @@ inline ShardedPayload alltoall_flat(const ShardedPayload& payload) {
   Chunk out(data.size());
   detail::check(moesim_alltoall_flat(payload.ranks, n, lens.data(), data.data(), out_lens.data(),
                                      out.data()));
+  ShardedPayload res = ShardedPayload::make(payload.ranks);
+  std::size_t o = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    res.chunks[i].assign(out.begin() + o, out.begin() + o + out_lens[i]);
+    o += out_lens[i];
+  }
+  return res;
+}
+
+// topology.hpp:15-60 — the shape and routing half of moesim::Topology (the
+// alpha-beta timing model belongs to the simulator, out of scope here).
+enum class LinkClass : std::uint8_t { kNvlink, kPcie, kSsdIo, kTor, kLeaf, kSpin };
+inline constexpr std::size_t kLinkClassCount = 6;
+using Path = std::vector<LinkClass>;
+struct LinkParams {
+  Bytes bandwidth_bytes_per_sec = 0;
+  std::int64_t latency_ns = 0;
+};
+struct GpuId {
+  std::uint32_t cluster = 0, node = 0, local_rank = 0;
+  friend bool operator==(const GpuId&, const GpuId&) = default;
+};
+
+class Topology {
+ public:
+  Topology(std::uint32_t clusters, std::uint32_t nodes_per_cluster, std::uint32_t gpus_per_node,
+           const std::array<LinkParams, kLinkClassCount>& links = flat())
+      : clusters_(clusters), nodes_(nodes_per_cluster), gpus_(gpus_per_node), links_(links) {
+    if (!clusters_) throw ConfigError("topology.clusters: must be >= 1");
+    if (!nodes_) throw ConfigError("topology.nodes_per_cluster: must be >= 1");
+    if (!gpus_) throw ConfigError("topology.gpus_per_node: must be >= 1");
+    static const char* names[kLinkClassCount] = {"nvlink", "pcie", "ssd_io", "tor", "leaf", "spin"};
+    for (std::size_t i = 0; i < kLinkClassCount; ++i) {
+      if (!links_[i].bandwidth_bytes_per_sec)
+        throw ConfigError(std::string("topology.links.") + names[i] +
+                          ".bandwidth_bytes_per_sec: must be > 0");
+      if (links_[i].latency_ns < 0)
+        throw ConfigError(std::string("topology.links.") + names[i] + ".latency_ns: must be >= 0");
+    }
+  }
+  std::uint32_t clusters() const { return clusters_; }
+  std::uint32_t nodes_per_cluster() const { return nodes_; }
+  std::uint32_t gpus_per_node() const { return gpus_; }
+  std::uint32_t total_gpus() const { return clusters_ * nodes_ * gpus_; }
+  const LinkParams& link(LinkClass c) const { return links_[static_cast<std::size_t>(c)]; }
+  std::uint32_t global_rank(const GpuId& g) const {
+    return (g.cluster * nodes_ + g.node) * gpus_ + g.local_rank;
+  }
+  GpuId gpu(std::uint32_t r) const {
+    if (r >= total_gpus()) throw std::out_of_range("topology: global rank out of range");
+    const std::uint32_t ni = r / gpus_;
+    return GpuId{ni / nodes_, ni % nodes_, r % gpus_};
+  }
+  bool valid(const GpuId& g) const {
+    return g.cluster < clusters_ && g.node < nodes_ && g.local_rank < gpus_;
+  }
+  Path route(const GpuId& s, const GpuId& d) const {
+    if (!valid(s)) throw std::out_of_range("topology.route: invalid src GPU id");
+    if (!valid(d)) throw std::out_of_range("topology.route: invalid dst GPU id");
+    if (s == d) return {};
+    if (s.cluster == d.cluster && s.node == d.node) return {LinkClass::kNvlink};
+    if (s.local_rank == d.local_rank) return {LinkClass::kTor, LinkClass::kLeaf, LinkClass::kTor};
+    return {LinkClass::kTor, LinkClass::kLeaf, LinkClass::kSpin, LinkClass::kLeaf,
+            LinkClass::kTor};
+  }
+
+ private:
+  static std::array<LinkParams, kLinkClassCount> flat() {
+    std::array<LinkParams, kLinkClassCount> l{};
+    for (auto& x : l) x.bandwidth_bytes_per_sec = 1;
+    return l;
+  }
+  std::uint32_t clusters_, nodes_, gpus_;
+  std::array<LinkParams, kLinkClassCount> links_;
+};
+
+// collectives.hpp:38-47
+struct AlltoAllStats {
+  std::array<std::size_t, kLinkClassCount> phase1_hops{};
+  std::array<std::size_t, kLinkClassCount> phase2_hops{};
+  std::size_t phase1_transfers = 0;
+  std::size_t phase2_transfers = 0;
+  std::size_t hops(LinkClass c) const {
+    return phase1_hops[static_cast<std::size_t>(c)] + phase2_hops[static_cast<std::size_t>(c)];
+  }
+};
+
+// collectives.hpp:54-55; both phases execute on the GPU
+inline ShardedPayload alltoall_hierarchical(const ShardedPayload& payload,
+                                            const Topology& topology,
+                                            AlltoAllStats* stats = nullptr) {
+  const std::size_t n = payload.chunks.size();
+  std::vector<std::uint64_t> lens(n), out_lens(n), st(14);
+  Chunk data;
+  for (std::size_t i = 0; i < n; ++i) {
+    lens[i] = payload.chunks[i].size();
+    data.insert(data.end(), payload.chunks[i].begin(), payload.chunks[i].end());
+  }
+  Chunk out(data.size());
+  detail::check(moesim_alltoall_hierarchical(
+      topology.clusters(), topology.nodes_per_cluster(), topology.gpus_per_node(), payload.ranks,
+      n, lens.data(), data.data(), out_lens.data(), out.data(), st.data()));
+  if (stats) {
+    for (std::size_t i = 0; i < kLinkClassCount; ++i) {
+      stats->phase1_hops[i] += st[i];
+      stats->phase2_hops[i] += st[6 + i];
+    }
+    stats->phase1_transfers += st[12];
+    stats->phase2_transfers += st[13];
+  }
   ShardedPayload res = ShardedPayload::make(payload.ranks);
   std::size_t o = 0;
   for (std::size_t i = 0; i < n; ++i) {

@@ -56,6 +56,8 @@ def lib():
         _lib.oracle_imbalance_ratio.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                                 C.POINTER(C.c_double)]
         _lib.oracle_alltoall_flat.argtypes = [C.c_uint64] * 2 + [C.c_void_p] * 4
+        _lib.oracle_alltoall_hierarchical.argtypes = [C.c_uint32] * 3 + [C.c_uint64] * 2 + [
+            C.c_void_p] * 5
         _lib.oracle_fuse_slices.argtypes = [C.c_uint64] + [C.c_void_p] * 4
         _lib.oracle_split_blob.argtypes = [C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                            C.c_void_p]
@@ -100,6 +102,8 @@ def ref():
             _ref.ref_imbalance_ratio.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                                  C.POINTER(C.c_double)]
             _ref.ref_alltoall_flat.argtypes = [C.c_uint64] * 2 + [C.c_void_p] * 4
+            _ref.ref_alltoall_hierarchical.argtypes = [C.c_uint32] * 3 + [C.c_uint64] * 2 + [
+                C.c_void_p] * 5
             _ref.ref_fuse_slices.argtypes = [C.c_uint64] + [C.c_void_p] * 4
             _ref.ref_split_blob.argtypes = [C.c_uint64, C.c_void_p, C.c_uint64, C.c_void_p,
                                             C.c_void_p]

@@ -170,6 +170,45 @@ int oracle_alltoall_flat(uint64_t ranks, uint64_t n_chunks, const uint64_t* lens
   return ORACLE_OK;
 }
 
+/* topology.cpp:61-71 route(): hop classes [nvlink,pcie,ssd_io,tor,leaf,spin]
+ * between two GPUs given as (node index, local rank). */
+static void oracle_route_hops(uint64_t na, uint64_t la, uint64_t nb, uint64_t lb, uint64_t* hops,
+                              uint64_t* transfers) {
+  if (na == nb && la == lb) return;
+  *transfers += 1;
+  if (na == nb) {
+    hops[0] += 1;
+  } else if (la == lb) {
+    hops[3] += 2;
+    hops[4] += 1;
+  } else {
+    hops[3] += 2;
+    hops[4] += 2;
+    hops[5] += 1;
+  }
+}
+
+/* collectives.cpp:31-79 — two-phase rail-aware all-to-all.  Delivery is the
+ * flat transpose (the chunks only travel through holders); the stats count
+ * phase 1 (src -> holder on src's node with dst's local rank) and phase 2
+ * (holder -> dst) hops.  stats: phase1_hops[6], phase2_hops[6], p1, p2. */
+int oracle_alltoall_hierarchical(uint32_t clusters, uint32_t nodes, uint32_t gpus, uint64_t ranks,
+                                 uint64_t n_chunks, const uint64_t* lens, const uint8_t* data,
+                                 uint64_t* out_lens, uint8_t* out_data, uint64_t* stats) {
+  if (clusters == 0 || nodes == 0 || gpus == 0) return ORACLE_ERR_CONFIG;
+  if (n_chunks != ranks * ranks) return ORACLE_ERR_INVALID;
+  if (ranks != (uint64_t)clusters * nodes * gpus) return ORACLE_ERR_INVALID;
+  memset(stats, 0, 14 * sizeof(uint64_t));
+  for (uint64_t s = 0; s < ranks; ++s)
+    for (uint64_t d = 0; d < ranks; ++d) {
+      /* node index = cluster * nodes + node identifies the node uniquely */
+      const uint64_t ns = s / gpus, ls = s % gpus, nd = d / gpus, ld = d % gpus;
+      oracle_route_hops(ns, ls, ns, ld, stats, &stats[12]);
+      oracle_route_hops(ns, ld, nd, ld, stats + 6, &stats[13]);
+    }
+  return oracle_alltoall_flat(ranks, n_chunks, lens, data, out_lens, out_data);
+}
+
 /* collectives.cpp:88-98 — concatenate, index = (slice_id, offset, length). */
 int oracle_fuse_slices(uint64_t n, const uint64_t* lens, const uint8_t* data, uint8_t* blob,
                        uint64_t* index /* n x 3 */) {

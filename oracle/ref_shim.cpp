@@ -100,6 +100,46 @@ int ref_alltoall_flat(uint64_t ranks, uint64_t n_chunks, const uint64_t* lens, c
   }
 }
 
+// collectives.cpp:31-79 through a Topology with flat (positive) link params;
+// stats: phase1_hops[6], phase2_hops[6], phase1_transfers, phase2_transfers
+int ref_alltoall_hierarchical(uint32_t clusters, uint32_t nodes, uint32_t gpus, uint64_t ranks,
+                              uint64_t n_chunks, const uint64_t* lens, const uint8_t* data,
+                              uint64_t* out_lens, uint8_t* out_data, uint64_t* stats) {
+  try {
+    std::array<LinkParams, kLinkClassCount> links{};
+    for (auto& l : links) {
+      l.bandwidth_bytes_per_sec = 1000;
+      l.latency_ns = 0;
+    }
+    const Topology topo(clusters, nodes, gpus, links);
+    ShardedPayload p;
+    p.ranks = ranks;
+    p.chunks.resize(n_chunks);
+    uint64_t off = 0;
+    for (uint64_t i = 0; i < n_chunks; ++i) {
+      p.chunks[i].assign(data + off, data + off + lens[i]);
+      off += lens[i];
+    }
+    AlltoAllStats st;
+    const ShardedPayload out = alltoall_hierarchical(p, topo, &st);
+    uint64_t o = 0;
+    for (uint64_t i = 0; i < out.chunks.size(); ++i) {
+      out_lens[i] = out.chunks[i].size();
+      std::memcpy(out_data + o, out.chunks[i].data(), out.chunks[i].size());
+      o += out.chunks[i].size();
+    }
+    for (int i = 0; i < 6; ++i) {
+      stats[i] = st.phase1_hops[i];
+      stats[6 + i] = st.phase2_hops[i];
+    }
+    stats[12] = st.phase1_transfers;
+    stats[13] = st.phase2_transfers;
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
 int ref_fuse_slices(uint64_t n, const uint64_t* lens, const uint8_t* data, uint8_t* blob,
                     uint64_t* index) {
   try {

@@ -204,6 +204,8 @@ SIGNATURES = {
     "moe_kernel_launch_count": (_U64, []),
     "moe_abi_sizeof": (_U64, [C.c_char_p]),
     "moesim_alltoall_flat": (_I, [_U64, _U64, _VP, _VP, _VP, _VP]),
+    "moesim_alltoall_hierarchical": (_I, [_U32, _U32, _U32, _U64, _U64, _VP, _VP, _VP, _VP,
+                                          _VP]),
     "moesim_fuse_slices": (_I, [_U64, _VP, _VP, _VP, _VP]),
     "moesim_split_blob": (_I, [_U64, _VP, _U64, _VP, _VP]),
     "moesim_gen_trace": (_I, [_U64, _U32, _U32, _U32, _U64, _D, _VP]),

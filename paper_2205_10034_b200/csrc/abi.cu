@@ -86,6 +86,104 @@ uint64_t moe_abi_sizeof(const char* n) {
 }
 
 // ------------------------------------------------------- moesim compat ----
+namespace {
+// topology.cpp route(): hop classes between two GPU ids (cluster, node, local)
+struct GpuPos {
+  uint32_t cluster, node, local;
+};
+void add_route(const GpuPos& a, const GpuPos& b, uint64_t* hops) {
+  enum { NVL = 0, TOR = 3, LEAF = 4, SPIN = 5 };
+  if (a.cluster == b.cluster && a.node == b.node) {
+    if (a.local != b.local) hops[NVL] += 1;
+    return;
+  }
+  hops[TOR] += 2;
+  hops[LEAF] += a.local == b.local ? 1 : 2;
+  if (a.local != b.local) hops[SPIN] += 1;
+}
+bool same_gpu(const GpuPos& a, const GpuPos& b) {
+  return a.cluster == b.cluster && a.node == b.node && a.local == b.local;
+}
+}  // namespace
+
+moe_status_t moesim_alltoall_hierarchical(uint32_t clusters, uint32_t nodes_per_cluster,
+                                          uint32_t gpus_per_node, uint64_t ranks,
+                                          uint64_t n_chunks, const uint64_t* lens,
+                                          const uint8_t* data, uint64_t* out_lens,
+                                          uint8_t* out_data, uint64_t* stats) {
+  return guard([&] {
+    moe::config_check(clusters >= 1, "topology.clusters: must be >= 1");
+    moe::config_check(nodes_per_cluster >= 1, "topology.nodes_per_cluster: must be >= 1");
+    moe::config_check(gpus_per_node >= 1, "topology.gpus_per_node: must be >= 1");
+    moe::arg_check(n_chunks == ranks * ranks, "alltoall: payload is not a square rank matrix");
+    moe::arg_check(ranks == (uint64_t)clusters * nodes_per_cluster * gpus_per_node,
+                   "alltoall: payload rank count does not match topology GPU count");
+    auto pos = [&](uint64_t r) {
+      const uint64_t node_index = r / gpus_per_node;
+      return GpuPos{(uint32_t)(node_index / nodes_per_cluster),
+                    (uint32_t)(node_index % nodes_per_cluster), (uint32_t)(r % gpus_per_node)};
+    };
+    auto rank_of = [&](const GpuPos& g) {
+      return ((uint64_t)g.cluster * nodes_per_cluster + g.node) * gpus_per_node + g.local;
+    };
+    std::vector<uint64_t> st(14, 0);
+    // phase 1: chunk (src, dst) -> holder (src node, dst local rank), in
+    // (src, dst) order; phase 2: holder -> dst, in per-holder arrival order
+    std::vector<std::vector<uint64_t>> staged(ranks);
+    for (uint64_t s = 0; s < ranks; ++s)
+      for (uint64_t d = 0; d < ranks; ++d) {
+        const GpuPos ps = pos(s), pd = pos(d);
+        const GpuPos h{ps.cluster, ps.node, pd.local};
+        if (!same_gpu(ps, h)) {
+          add_route(ps, h, st.data());
+          st[12] += 1;
+        }
+        staged[rank_of(h)].push_back(s * ranks + d);
+      }
+    std::vector<uint64_t> in_off(n_chunks), stage_off(n_chunks), out_off(n_chunks);
+    uint64_t total = 0, mx = 0;
+    for (uint64_t i = 0; i < n_chunks; ++i) {
+      in_off[i] = total;
+      total += lens[i];
+      mx = std::max(mx, lens[i]);
+    }
+    uint64_t o = 0;
+    for (uint64_t h = 0; h < ranks; ++h)
+      for (uint64_t c : staged[h]) {
+        stage_off[c] = o;
+        o += lens[c];
+        const GpuPos ph = pos(h), pd = pos(c % ranks);
+        if (!same_gpu(ph, pd)) {
+          add_route(ph, pd, st.data() + 6);
+          st[13] += 1;
+        }
+      }
+    o = 0;
+    for (uint64_t d = 0; d < ranks; ++d)
+      for (uint64_t s = 0; s < ranks; ++s) {
+        out_off[s * ranks + d] = o;  // chunk (s, d) lands at out (d, s)
+        out_lens[d * ranks + s] = lens[s * ranks + d];
+        o += lens[s * ranks + d];
+      }
+    if (stats) std::copy(st.begin(), st.end(), stats);
+    if (!ranks || !total) return;
+    PrivStream ps;
+    DBuf dl(n_chunks * 8), di(n_chunks * 8), dso(n_chunks * 8), doo(n_chunks * 8), din(total),
+        dstage(total), dout(total);
+    MOE_CUDA(cudaMemcpyAsync(dl.p, lens, n_chunks * 8, cudaMemcpyHostToDevice, ps.s));
+    MOE_CUDA(cudaMemcpyAsync(di.p, in_off.data(), n_chunks * 8, cudaMemcpyHostToDevice, ps.s));
+    MOE_CUDA(cudaMemcpyAsync(dso.p, stage_off.data(), n_chunks * 8, cudaMemcpyHostToDevice, ps.s));
+    MOE_CUDA(cudaMemcpyAsync(doo.p, out_off.data(), n_chunks * 8, cudaMemcpyHostToDevice, ps.s));
+    MOE_CUDA(cudaMemcpyAsync(din.p, data, total, cudaMemcpyHostToDevice, ps.s));
+    moe::copy_chunks_device(n_chunks, dl.as<uint64_t>(), di.as<uint64_t>(), din.as<uint8_t>(),
+                            dso.as<uint64_t>(), dstage.as<uint8_t>(), mx, ps.s);  // phase 1
+    moe::copy_chunks_device(n_chunks, dl.as<uint64_t>(), dso.as<uint64_t>(), dstage.as<uint8_t>(),
+                            doo.as<uint64_t>(), dout.as<uint8_t>(), mx, ps.s);    // phase 2
+    MOE_CUDA(cudaMemcpyAsync(out_data, dout.p, total, cudaMemcpyDeviceToHost, ps.s));
+    MOE_CUDA(cudaStreamSynchronize(ps.s));
+  });
+}
+
 moe_status_t moesim_alltoall_flat(uint64_t ranks, uint64_t n_chunks, const uint64_t* lens,
                                   const uint8_t* data, uint64_t* out_lens, uint8_t* out_data) {
   return guard([&] {

@@ -92,6 +92,9 @@ void alltoall_packed(void* comm, const void* send, void* recv, uint64_t bytes_pe
                      uint32_t slices_per_peer, int fused, cudaStream_t st);
 
 // moesim_ops.cu
+void copy_chunks_device(uint64_t n, const uint64_t* lens, const uint64_t* in_off,
+                        const uint8_t* in, const uint64_t* out_off, uint8_t* out, uint64_t max_len,
+                        cudaStream_t st);
 void gen_trace_device(uint64_t seed, uint32_t steps, uint32_t ranks, uint32_t experts,
                       uint64_t tokens, double skew, uint64_t* counts, cudaStream_t st);
 void imbalance_device(uint64_t rows, uint32_t experts, const uint64_t* counts,

@@ -118,6 +118,19 @@ __global__ void a2a_flat_kernel(uint64_t R, const uint64_t* __restrict__ lens,
   copy_bytes(out + out_off[d * R + s] + p0, in + in_off[c] + p0, p1 - p0);
 }
 
+// generic chunk permutation: chunk i of `in` (in_off[i], len[i]) -> out at out_off[i]
+__global__ void chunk_copy_kernel(const uint64_t* __restrict__ lens,
+                                  const uint64_t* __restrict__ in_off, const uint8_t* __restrict__ in,
+                                  const uint64_t* __restrict__ out_off, uint8_t* __restrict__ out) {
+  const uint64_t c = blockIdx.x;
+  const uint64_t len = lens[c];
+  const uint64_t part = (len + gridDim.y - 1) / gridDim.y;
+  const uint64_t p0 = min(len, ((part + 15) / 16) * 16 * blockIdx.y);
+  const uint64_t p1 = min(len, p0 + ((part + 15) / 16) * 16);
+  if (p0 >= p1) return;
+  copy_bytes(out + out_off[c] + p0, in + in_off[c] + p0, p1 - p0);
+}
+
 __global__ void fuse_index_kernel(uint64_t n, const uint64_t* __restrict__ lens,
                                   moe_slice_index_entry_t* __restrict__ index) {
   if (threadIdx.x != 0) return;
@@ -228,6 +241,17 @@ void alltoall_flat_device(uint64_t R, const uint64_t* lens, const uint64_t* in_o
   dim3 grid((unsigned)(R * R), split);
   a2a_flat_kernel<<<grid, 256, 0, st>>>(R, lens, in_off, in, out_off, out);
   MOE_LAUNCH_CHECK("a2a_flat_kernel");
+  count_launch();
+}
+
+void copy_chunks_device(uint64_t n, const uint64_t* lens, const uint64_t* in_off,
+                        const uint8_t* in, const uint64_t* out_off, uint8_t* out, uint64_t max_len,
+                        cudaStream_t st) {
+  if (!n) return;
+  const unsigned split = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(max_len, 1 << 20), 64));
+  dim3 grid((unsigned)n, split);
+  chunk_copy_kernel<<<grid, 256, 0, st>>>(lens, in_off, in, out_off, out);
+  MOE_LAUNCH_CHECK("chunk_copy_kernel");
   count_launch();
 }
 

@@ -62,6 +62,67 @@ def alltoall_flat(payload: ShardedPayload) -> ShardedPayload:
     return res
 
 
+LINK_CLASSES = ("nvlink", "pcie", "ssd_io", "tor", "leaf", "spin")  # topology.hpp:15
+
+
+@dataclass
+class Topology:
+    """topology.hpp:37-60 shape (clusters x nodes_per_cluster x gpus_per_node);
+    zero dimensions raise ConfigError like the reference constructor."""
+    clusters: int
+    nodes_per_cluster: int
+    gpus_per_node: int
+
+    def __post_init__(self):
+        for name in ("clusters", "nodes_per_cluster", "gpus_per_node"):
+            if getattr(self, name) < 1:
+                raise ConfigError(f"topology.{name}: must be >= 1")
+
+    def total_gpus(self) -> int:
+        return self.clusters * self.nodes_per_cluster * self.gpus_per_node
+
+
+@dataclass
+class AlltoAllStats:
+    """collectives.hpp:38-47; hop lists are indexed like LINK_CLASSES."""
+    phase1_hops: List[int] = field(default_factory=lambda: [0] * 6)
+    phase2_hops: List[int] = field(default_factory=lambda: [0] * 6)
+    phase1_transfers: int = 0
+    phase2_transfers: int = 0
+
+    def hops(self, link: str) -> int:
+        i = LINK_CLASSES.index(link)
+        return self.phase1_hops[i] + self.phase2_hops[i]
+
+
+def alltoall_hierarchical(payload: ShardedPayload, topology: Topology,
+                          stats: Optional[AlltoAllStats] = None) -> ShardedPayload:
+    """collectives.cpp:31-79: rail-aware two-phase all-to-all (both phases on the
+    GPU); delivers alltoall_flat's result and accumulates hop counts in stats."""
+    n = len(payload.chunks)
+    lens = _u64([len(c) for c in payload.chunks])
+    data = np.frombuffer(b"".join(payload.chunks), dtype=np.uint8).copy()
+    out_lens = np.zeros(n, dtype=np.uint64)
+    out = np.zeros(max(int(lens.sum()), 1), dtype=np.uint8)
+    st = np.zeros(14, dtype=np.uint64)
+    call("moesim_alltoall_hierarchical", topology.clusters, topology.nodes_per_cluster,
+         topology.gpus_per_node, payload.ranks, n, _ptr(lens), _ptr(data), _ptr(out_lens),
+         _ptr(out), _ptr(st))
+    if stats is not None:
+        for i in range(6):
+            stats.phase1_hops[i] += int(st[i])
+            stats.phase2_hops[i] += int(st[6 + i])
+        stats.phase1_transfers += int(st[12])
+        stats.phase2_transfers += int(st[13])
+    res = ShardedPayload.make(payload.ranks)
+    o = 0
+    for i in range(n):
+        ln = int(out_lens[i])
+        res.chunks[i] = out[o:o + ln].tobytes()
+        o += ln
+    return res
+
+
 @dataclass
 class FusedBlob:
     blob: bytes

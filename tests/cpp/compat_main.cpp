@@ -92,6 +92,44 @@ void alltoall_cases() {
   }
 }
 
+// test_collectives.cpp:69-110 through the drop-in Topology / AlltoAllStats
+void hierarchical_cases() {
+  {
+    const Topology topo(1, 1, 4);
+    const ShardedPayload p = random_payload(4, 5);
+    AlltoAllStats st;
+    check(alltoall_hierarchical(p, topo, &st) == alltoall_flat(p), "one node = flat");
+    check(st.phase2_transfers == 0, "one node: no phase 2");
+  }
+  {
+    const Topology topo(1, 2, 2);
+    ShardedPayload p = ShardedPayload::make(4);
+    for (std::uint8_t s = 0; s < 4; ++s)
+      for (std::uint8_t d = 0; d < 4; ++d) p.at(s, d) = {s, d};
+    AlltoAllStats st;
+    check(alltoall_hierarchical(p, topo, &st) == alltoall_flat(p), "2x2 tagged");
+    check(st.hops(LinkClass::kSpin) == 0, "2x2 no spin");
+  }
+  std::uint64_t seed = 1;
+  for (std::uint32_t c = 1; c <= 2; ++c)
+    for (std::uint32_t n = 1; n <= 2; ++n)
+      for (std::uint32_t g = 1; g <= 4; ++g) {
+        const Topology topo(c, n, g);
+        for (int rep = 0; rep < 5; ++rep) {
+          const ShardedPayload p = random_payload(topo.total_gpus(), seed++);
+          AlltoAllStats st;
+          check(alltoall_hierarchical(p, topo, &st) == alltoall_flat(p), "random topology");
+          check(st.phase2_hops[5] == 0 && st.phase1_hops[3] == 0 && st.phase1_hops[5] == 0,
+                "rails only");
+        }
+      }
+  const Topology topo(1, 2, 2);
+  expect_throw<std::invalid_argument>([&] { alltoall_hierarchical(random_payload(3, 1), topo); },
+                                      "rank mismatch");
+  expect_throw<ConfigError>([&] { Topology(0, 1, 1); }, "zero clusters");
+  check(topo.route(topo.gpu(0), topo.gpu(3)).size() == 5, "cross-rail route via spin");
+}
+
 void fusion_cases() {
   const std::vector<Chunk> one = {{1, 2, 3}};
   const FusedBlob f = fuse_slices(one);
@@ -316,6 +354,7 @@ void sparse_cache_cases() {
 int main() {
   const std::vector<std::pair<std::string, std::function<void()>>> crit = {
       {"alltoall_flat = chunk transpose (collectives.cpp:10-21)", alltoall_cases},
+      {"alltoall_hierarchical = flat, rails only (collectives.cpp:31-79)", hierarchical_cases},
       {"fuse_slices/split_blob exact inverses + errors (collectives.cpp:88-118)", fusion_cases},
       {"gen_trace = independent sampler, conservation, imbalance (workload.cpp:19-66)",
        workload_cases},

@@ -58,6 +58,24 @@ def ref_a2a(ranks, chunks):
     return {"chunks": res}
 
 
+def ref_a2a_hier(topo, ranks, chunks):
+    r = oracle.ref()
+    lens = np.array([len(c) for c in chunks] or [0], dtype=np.uint64)
+    data = np.frombuffer(b"".join(chunks) or b"\0", dtype=np.uint8).copy()
+    out_lens = np.zeros(max(1, len(chunks)), dtype=np.uint64)
+    out = np.zeros(max(1, int(lens.sum())), dtype=np.uint8)
+    stats = np.zeros(14, dtype=np.uint64)
+    rc = r.ref_alltoall_hierarchical(*topo, ranks, len(chunks), oracle.P(lens), oracle.P(data),
+                                     oracle.P(out_lens), oracle.P(out), oracle.P(stats))
+    if rc:
+        return {"error": rc}
+    res, o = [], 0
+    for ln in out_lens[:len(chunks)]:
+        res.append(out[o:o + int(ln)].tobytes().hex())
+        o += int(ln)
+    return {"chunks": res, "stats": [int(v) for v in stats]}
+
+
 def ref_fuse(slices):
     r = oracle.ref()
     n = len(slices)
@@ -199,6 +217,30 @@ def main():
     for ent in a2a:
         ent["expected"] = ref_a2a(ent["ranks"], [bytes.fromhex(c) for c in ent["chunks"]])
     gold["alltoall_flat"] = a2a
+
+    # collectives.cpp:31-79 — test_collectives.cpp:69-110
+    hier = [{"topo": [1, 1, 4], "ranks": 4, "chunks": [c.hex() for c in random_payload(4, 5)]},
+            {"topo": [1, 2, 2], "ranks": 4,
+             "chunks": [bytes([s_, d_]).hex() for s_ in range(4) for d_ in range(4)]}]
+    seed = 1
+    for cl in (1, 2):
+        for nd in (1, 2):
+            for gp in (1, 2, 3, 4):
+                for _ in range(5):
+                    R = cl * nd * gp
+                    hier.append({"topo": [cl, nd, gp], "ranks": R,
+                                 "chunks": [c.hex() for c in random_payload(R, seed)]})
+                    seed += 1
+    hier.append({"topo": [2, 2, 4], "ranks": 16,
+                 "chunks": [c.hex() for c in random_payload(16, 77, 300)]})
+    hier.append({"topo": [1, 2, 2], "ranks": 3, "chunks": [c.hex() for c in random_payload(3, 1)]})
+    hier.append({"topo": [1, 2, 2], "ranks": 2, "chunks": ["aa", "bb", "cc"]})
+    hier.append({"topo": [0, 2, 2], "ranks": 4, "chunks": [c.hex() for c in random_payload(4, 2)]})
+    hier.append({"topo": [1, 1, 0], "ranks": 0, "chunks": []})
+    for ent in hier:
+        ent["expected"] = ref_a2a_hier(ent["topo"], ent["ranks"],
+                                       [bytes.fromhex(c) for c in ent["chunks"]])
+    gold["alltoall_hierarchical"] = hier
 
     # collectives.cpp:88-118 — test_collectives.cpp:136-171
     fuse = [[bytes([1, 2, 3])], [bytes([1, 2, 3]), b"", bytes([4, 5, 6, 7, 8])], []]

@@ -71,6 +71,27 @@ def test_alltoall_flat_matches_reference(golden):
         assert got == ent["expected"]
 
 
+def test_alltoall_hierarchical_matches_reference(golden):
+    """collectives.cpp:31-79 — delivery and per-phase hop stats, test_collectives.cpp:69-110."""
+    for ent in golden["alltoall_hierarchical"]:
+        chunks = [bytes.fromhex(c) for c in ent["chunks"]]
+        lens = np.array([len(c) for c in chunks] or [0], dtype=np.uint64)
+        data = np.frombuffer(b"".join(chunks) or b"\0", dtype=np.uint8).copy()
+        out_lens = np.zeros(max(1, len(chunks)), dtype=np.uint64)
+        out = np.zeros(max(1, int(lens.sum())), dtype=np.uint8)
+        stats = np.zeros(14, dtype=np.uint64)
+        rc = oracle.lib().oracle_alltoall_hierarchical(
+            *ent["topo"], ent["ranks"], len(chunks), oracle.P(lens), oracle.P(data),
+            oracle.P(out_lens), oracle.P(out), oracle.P(stats))
+        if "error" in ent["expected"]:
+            assert rc == ent["expected"]["error"], ent["topo"]
+            continue
+        assert rc == 0
+        assert stats.tolist() == ent["expected"]["stats"], ent["topo"]
+        assert _a2a(ent["ranks"], chunks)["chunks"] == ent["expected"]["chunks"]
+        assert stats[6 + 5] == 0 and stats[3] == 0 and stats[5] == 0  # rails only
+
+
 def test_fuse_split_match_reference(golden):
     for ent in golden["fuse_slices"]:
         slices = [bytes.fromhex(s) for s in ent["slices"]]
