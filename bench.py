@@ -365,13 +365,25 @@ def main():
             "traffic": traffic, "peak_source": psrc,
             "flops_per_step": flops_step, "gemm_ms_per_step": gemm_ms,
             "gemm_share_of_step": gemm_ms / ms_step if ms_step else None}
-    # per-GEMM view: each of the six carries 2 * rows * d * d_ff flops
+    # per-GEMM view: each of the six carries 2 * rows * d * d_ff flops; its
+    # algorithmic HBM bytes are its operands + outputs once:
+    # activations R x {d, d_ff}, weights E_local x d x d_ff, fp32 dW
+    es = 2 if dtype == torch.bfloat16 else 4
+    R, W = rows_local, (E // ws) * d * dff
+    gbytes = {"ffn1": es * (R * d + W + 2 * R * dff),          # X, W1 -> A, gelu'(h)
+              "ffn2": es * (R * dff + W + R * d),              # A, W2 -> Y
+              "dgrad_ffn2": es * (R * d + W + 2 * R * dff),    # dY, W2, gelu'(h) -> dH
+              "dgrad_ffn1": es * (R * dff + W + R * d),        # dH, W1 -> dX
+              "wgrad_w1": es * (R * d + R * dff) + 4 * W,      # X, dH -> dW1 (fp32)
+              "wgrad_w2": es * (R * dff + R * d) + 4 * W}      # A, dY -> dW2 (fp32)
     per = []
     for name in ("ffn1", "ffn2", "dgrad_ffn2", "dgrad_ffn1", "wgrad_w1", "wgrad_w2"):
         ms_k = sum(v for n, v in phase_tot.items() if n.split(".", 1)[-1] == name) / args.steps
         if ms_k > 0:
             tf = 2.0 * rows_local * d * dff / (ms_k / 1000.0) / 1e12
-            per.append({"gemm": name, "ms": ms_k, "tflops": tf, "frac": tf / peak})
+            gbs = gbytes[name] / (ms_k / 1000.0) / 1e9
+            per.append({"gemm": name, "ms": ms_k, "tflops": tf, "frac": tf / peak,
+                        "hbm_GBps": gbs, "hbm_frac": gbs / pk["hbm_gbs"]})
     roof["per_gemm"] = per
 
     # ---- end to end through the host-buffer API (H2D + step + D2H) ----

@@ -301,6 +301,49 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(Win w, uint64_t home_off,
   grid_done_signal(w, ctr, slot_id, epoch);
 }
 
+// red[me] of every window := a ++ b (float4 stores over NVLink for a)
+__global__ void p2p_red_push_kernel(Win w, uint64_t off_red, uint64_t n_red, uint32_t* ctr,
+                                    const float* __restrict__ a, uint64_t na,
+                                    const float* __restrict__ b, uint64_t nb, uint64_t epoch) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid; i < na / 4; i += nt) {
+    const float4 v = reinterpret_cast<const float4*>(a)[i];
+    for (uint32_t p = 0; p < w.P; ++p)
+      reinterpret_cast<float4*>(w.peers[p] + off_red + (uint64_t)w.me * n_red * 4)[i] = v;
+  }
+  for (uint64_t i = tid; i < nb; i += nt) {
+    const float v = b[i];
+    for (uint32_t p = 0; p < w.P; ++p)
+      reinterpret_cast<float*>(w.peers[p] + off_red + (uint64_t)w.me * n_red * 4)[na + i] = v;
+  }
+  grid_done_signal(w, ctr, SLOT_GRAD, epoch);
+}
+
+// a ++ b := sum over sources of red[s], in source order (identical on all ranks)
+__global__ void p2p_red_sum_kernel(const float* __restrict__ red, uint32_t P, uint64_t n_red,
+                                   float* __restrict__ a, uint64_t na, float* __restrict__ b,
+                                   uint64_t nb) {
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = tid; i < na / 4; i += nt) {
+    float4 acc = reinterpret_cast<const float4*>(red)[i];
+    for (uint32_t s = 1; s < P; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(red + s * n_red)[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(a)[i] = acc;
+  }
+  for (uint64_t i = tid; i < nb; i += nt) {
+    float acc = red[na + i];
+    for (uint32_t s = 1; s < P; ++s) acc += red[s * n_red + na + i];
+    b[i] = acc;
+  }
+}
+
 uint64_t a256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 
 Win win_of(const P2PWindow& w) {
@@ -321,7 +364,7 @@ uint32_t* ctr_of(const P2PWindow& w, int i) {
   } while (0)
 
 void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t E, uint64_t Cs,
-               uint64_t row_bytes, cudaStream_t st) {
+               uint64_t row_bytes, uint64_t n_red, cudaStream_t st) {
   config_check(P <= 8, "layer.ep_size: P2P exchange supports up to 8 GPUs of one box");
   config_check(E <= (uint32_t)MAXE, "layer.num_experts: P2P exchange supports up to 256");
   config_check(row_bytes % 16 == 0, "layer.d_model: rows must be a multiple of 16 bytes");
@@ -332,6 +375,7 @@ void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t 
   w.Cs = Cs;
   w.Rmax = (uint64_t)P * Cs;
   w.row_bytes = row_bytes;
+  w.n_red = (n_red + 3) / 4 * 4;
   const uint64_t region = (uint64_t)w.El * w.Rmax * row_bytes;  // == E * Cs rows
   const uint64_t home = (uint64_t)E * Cs * row_bytes;
   w.off_xr = 0;
@@ -341,7 +385,8 @@ void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t 
   w.off_cnt = a256(w.off_dxh + home);
   w.off_flags = a256(w.off_cnt + (uint64_t)P * E * 4);
   w.off_ctr = a256(w.off_flags + (uint64_t)NSLOT * P * 8);
-  w.bytes = w.off_ctr + 256;
+  w.off_red = a256(w.off_ctr + 256);
+  w.bytes = w.off_red + (uint64_t)P * w.n_red * 4;
   MOE_CUDA(cudaMalloc(&w.base, w.bytes));
   MOE_CUDA(cudaMemsetAsync(w.base, 0, w.bytes, st));
   MOE_CUDA(cudaMalloc(&w.err, sizeof(int32_t)));
@@ -402,6 +447,23 @@ void p2p_signal(const P2PWindow& w, int slot, uint64_t value, cudaStream_t st) {
 void p2p_counts(const P2PWindow& w, const int32_t* kept, uint64_t epoch, cudaStream_t st) {
   p2p_counts_kernel<<<1, 256, 0, st>>>(win_of(w), ctr_of(w, 4), kept, epoch);
   MOE_LAUNCH_CHECK("p2p_counts_kernel");
+  count_launch();
+}
+
+void p2p_allreduce_f32(const P2PWindow& w, float* a, uint64_t na, float* b, uint64_t nb,
+                       uint64_t epoch, cudaStream_t st) {
+  if (w.P <= 1) return;
+  arg_check(na % 4 == 0 && na + nb <= w.n_red, "p2p_allreduce: gradient does not fit the window");
+  const unsigned grid = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>(ceil_div(na / 4 + nb, 256), (uint64_t)num_sms()));
+  p2p_red_push_kernel<<<grid, 256, 0, st>>>(win_of(w), w.off_red, w.n_red, ctr_of(w, 5), a, na,
+                                            b, nb, epoch);
+  MOE_LAUNCH_CHECK("p2p_red_push_kernel");
+  count_launch();
+  p2p_wait(w, SLOT_GRAD, epoch, st);
+  p2p_red_sum_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(w.base + w.off_red),
+                                           w.P, w.n_red, a, na, b, nb);
+  MOE_LAUNCH_CHECK("p2p_red_sum_kernel");
   count_launch();
 }
 

@@ -17,7 +17,8 @@ enum P2PSlot : int {
   SLOT_Y = 3,         // src pushed our expert outputs into our home Y
   SLOT_DY = 4,        // src's g*dy rows are in our recv_dy
   SLOT_DX = 5,        // src pushed our dX rows into our home dX
-  NSLOT = 6
+  SLOT_GRAD = 6,      // src's replicated-gradient partials are in our red[src]
+  NSLOT = 7
 };
 
 // One cudaMalloc per rank holding everything peers write into; mapped into
@@ -28,20 +29,22 @@ enum P2PSlot : int {
 //                      expert GEMM sees ONE group per expert for any P
 //   home_y / home_dx : [E][Cs][d], rows returned to their source positions
 //   cnt              : [P][E] kept counts of every source (all-gathered)
+//   red              : [P][n_red] fp32 partials of the replicated (gate)
+//                      gradients, one row per source
 struct P2PWindow {
   uint32_t P = 1, me = 0, E = 0, El = 0;
-  uint64_t Cs = 0, Rmax = 0, row_bytes = 0;
+  uint64_t Cs = 0, Rmax = 0, row_bytes = 0, n_red = 0;
   uint8_t* base = nullptr;
   uint64_t bytes = 0;
   uint64_t off_xr = 0, off_dyr = 0, off_yh = 0, off_dxh = 0, off_cnt = 0, off_flags = 0,
-           off_ctr = 0;
+           off_ctr = 0, off_red = 0;
   uint8_t* peer_host[8] = {};
   uint8_t** peer_dev = nullptr;
   int32_t* err = nullptr;
 };
 
 void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t E, uint64_t Cs,
-               uint64_t row_bytes, cudaStream_t st);
+               uint64_t row_bytes, uint64_t n_red, cudaStream_t st);
 void p2p_teardown(P2PWindow& w);
 
 // Wait until flags[slot][src] >= target for every src != me (device spin with
@@ -77,5 +80,13 @@ void p2p_combine_bwd(const P2PWindow& w, uint64_t T, uint32_t d, uint32_t k, moe
 // [(me*El + j)*Cs + r]; then `slot` := epoch at every peer.
 void p2p_push_home(const P2PWindow& w, uint64_t home_off, const void* src, int slot,
                    uint64_t epoch, cudaStream_t st);
+
+// Sum-all-reduce of replicated fp32 gradients (a[0:na] ++ b[0:nb], na % 4 ==
+// 0, na + nb <= n_red) over peer memory: every rank stores its partial into
+// red[me] of every window (SLOT_GRAD := epoch), then sums red[0..P-1] in rank
+// order, so all replicas end bitwise identical.  Replaces ncclAllReduce for
+// the small gate gradients (latency, not bandwidth, bound).
+void p2p_allreduce_f32(const P2PWindow& w, float* a, uint64_t na, float* b, uint64_t nb,
+                       uint64_t epoch, cudaStream_t st);
 
 }  // namespace moe

@@ -111,7 +111,7 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
                "layer.exchange: must be MOE_EXCHANGE_P2P or MOE_EXCHANGE_NCCL");
   if (p2p) {
     // receive / home buffers live in one IPC window that every peer maps
-    p2p_setup(win, comm, P, rank, E, Cs, (uint64_t)dm * esz, 0);
+    p2p_setup(win, comm, P, rank, E, Cs, (uint64_t)dm * esz, (uint64_t)E * dm + E, 0);
     xr = win.base + win.off_xr;
     dYr = win.base + win.off_dyr;
     Yh = win.base + win.off_yh;
@@ -531,7 +531,11 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("gate_wgrad", st);
-  if (P > 1) {
+  if (p2p) {
+    // replicated gate gradients: one-shot all-reduce over the peer windows
+    p2p_allreduce_f32(win, g.dwg, (uint64_t)E * dm, desc.has_gate_bias ? g.dbg : nullptr,
+                      desc.has_gate_bias && g.dbg ? E : 0, ph, st);
+  } else if (P > 1) {
     MOE_NCCL(ncclGroupStart());
     MOE_NCCL(ncclAllReduce(g.dwg, g.dwg, (uint64_t)E * dm, ncclFloat32, ncclSum, (ncclComm_t)comm, st));
     if (desc.has_gate_bias && g.dbg)

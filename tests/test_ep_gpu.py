@@ -102,6 +102,10 @@ def _worker(rank, world, port, case, q):
             assert err < 2e-3, (n, err.item())
         err = (lep.grads["dwg"] - g1["dwg"]).abs().max() / g1["dwg"].abs().max()
         assert err < 1e-4, ("dwg", err.item())
+        # the replicated gate gradient is bitwise identical on every rank
+        allg = [torch.empty_like(lep.grads["dwg"]) for _ in range(world)]
+        dist.all_gather(allg, lep.grads["dwg"].contiguous())
+        assert all(torch.equal(allg[0], t) for t in allg[1:]), "dwg replicas differ"
         lep.close()
         ep.close()
         dist.destroy_process_group()
