@@ -393,8 +393,13 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   }
   else if (P > 1) a2a(dYs, dYr, El * Cs * dm * esz, st);
   mark("a2a_dy", st);
+  // db2 = column sums of dY, while dY is still warm in L2 (after the weight
+  // gradients the L2 is full of dirty fp32 dW lines and every read pays a
+  // write-back)
+  group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs);
+  mark("bias_grads", st);
   // Weight-gradient GEMMs (RAGGED_K over the slices of each expert):
-  // dW1[j] = sum dH^T X, dW2[j] = sum dY^T A; db2 = column sums of dY.
+  // dW1[j] = sum dH^T X, dW2[j] = sum dY^T A.
   auto wgrad = [&](bool w1, cudaStream_t s) {
     moe_gemm_problem_t p;
     std::memset(&p, 0, sizeof(p));
@@ -472,8 +477,6 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   mark("wgrad_w1", st);
   wgrad(false, st);
   mark("wgrad_w2", st);
-  group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs);
-  mark("bias_grads", st);
   if (p2p) p2p_wait(win, SLOT_DX, ph, st);
   // gate dgrad with the combine backward folded into its epilogue:
   // dx[t] = dlogits[t] wg + sum_i dXe[slot_i]; dwg = dlogits^T x (split-K)

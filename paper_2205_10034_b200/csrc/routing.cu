@@ -669,7 +669,7 @@ __global__ void colsum_kernel(const int32_t* __restrict__ gm, const int32_t* __r
   atomicAdd(out + (uint64_t)gb[g] * N + n, s);
 }
 
-// bf16, 8 columns per thread (16-byte loads), 64 rows per block, 4 rows in flight
+// bf16, 8 columns per thread (16-byte loads), 64 rows per block, 8 rows in flight
 __global__ void colsum_bf16x8_kernel(const int32_t* __restrict__ gm, const int32_t* __restrict__ ga,
                                      const int32_t* __restrict__ gb, int N,
                                      const __nv_bfloat16* __restrict__ X, float* __restrict__ out) {
@@ -683,12 +683,12 @@ __global__ void colsum_bf16x8_kernel(const int32_t* __restrict__ gm, const int32
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const __nv_bfloat16* base = X + ((uint64_t)ga[g] + r0) * N + n;
   int r = r0;
-  for (; r + 4 <= r1; r += 4, base += 4 * (uint64_t)N) {
-    uint4 v[4];
+  for (; r + 8 <= r1; r += 8, base += 8 * (uint64_t)N) {
+    uint4 v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)u * N));
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)u * N));
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v[u]);
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
@@ -703,6 +703,62 @@ __global__ void colsum_bf16x8_kernel(const int32_t* __restrict__ gm, const int32
   float* o = out + (uint64_t)gb[g] * N + n;
 #pragma unroll
   for (int q = 0; q < 8; ++q) atomicAdd(o + q, acc[q]);
+}
+
+// One group per output row (groups == num_b): a block per (group, 256-column
+// slice) sums ALL the group's rows — 16 row lanes x 32 column threads (8 bf16
+// columns each), 8 rows in flight per thread — and reduces the row lanes in a
+// fixed order through shared memory: deterministic, no atomics, no memset.
+constexpr int CS_LANES = 16;
+__global__ void __launch_bounds__(CS_LANES * 32) colsum_group_bf16_kernel(
+    const int32_t* __restrict__ gm, const int32_t* __restrict__ ga, const int32_t* __restrict__ gb,
+    int N, const __nv_bfloat16* __restrict__ X, float* __restrict__ out) {
+  __shared__ float part[CS_LANES][256 + 8];
+  const int g = blockIdx.x;
+  const int rows = gm[g];
+  const int cl = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int n = blockIdx.y * 256 + cl * 8;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (n < N) {
+    const __nv_bfloat16* base = X + (uint64_t)ga[g] * N + n;
+    int r = rl;
+    for (; r + 7 * CS_LANES < rows; r += 8 * CS_LANES) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)(r + u * CS_LANES) * N));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(h[q]);
+          acc[2 * q] += f.x;
+          acc[2 * q + 1] += f.y;
+        }
+      }
+    }
+    for (; r < rows; r += CS_LANES) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)r * N));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(h[q]);
+        acc[2 * q] += f.x;
+        acc[2 * q + 1] += f.y;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) part[rl][cl * 8 + q] = acc[q];
+  __syncthreads();
+  if (threadIdx.x < 256) {
+    const int col = blockIdx.y * 256 + threadIdx.x;
+    float sum = 0.f;
+#pragma unroll
+    for (int l = 0; l < CS_LANES; ++l) sum += part[l][threadIdx.x];
+    if (col < N) out[(uint64_t)gb[g] * N + col] = sum;
+  }
 }
 
 __global__ void build_groups_kernel(uint32_t P, uint32_t El, uint64_t Cs, const int32_t* cnt,
@@ -827,6 +883,14 @@ void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, con
 void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const int32_t* gb,
                   uint32_t num_b, uint32_t N, moe_dtype_t dt, const void* X, float* out,
                   cudaStream_t st, uint64_t max_rows) {
+  if (dt == MOE_DTYPE_BF16 && N % 8 == 0 && groups == num_b) {
+    // one group per expert (N = 1 and the P2P exchange): gb is a permutation
+    colsum_group_bf16_kernel<<<dim3(groups, (unsigned)ceil_div(N, 256)), CS_LANES * 32, 0, st>>>(
+        gm, ga, gb, (int)N, (const __nv_bfloat16*)X, out);
+    MOE_LAUNCH_CHECK("colsum_group_bf16_kernel");
+    count_launch();
+    return;
+  }
   MOE_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (uint64_t)num_b * N, st));
   if (dt == MOE_DTYPE_BF16 && N % 8 == 0) {
     dim3 grid(groups, (unsigned)ceil_div(max_rows, 64), (unsigned)ceil_div(N / 8, 128));
