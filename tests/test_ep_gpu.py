@@ -51,6 +51,34 @@ def _worker(rank, world, port, case, q):
                     assert torch.equal(recv[s * nn:(s + 1) * nn], allsend[s][rank * n:rank * n + nn])
             q.put((rank, "ok"))
             return
+        if case == "a2a_timing":
+            # test_collectives.cpp:235-255 on real NVLink: the same bytes as one
+            # fused message per peer or as k slices; the fused exchange pays the
+            # per-message latency once and is never slower
+            slice_bytes = 4096
+            res = {}
+            for kk in (1, 2, 4, 8):
+                n = kk * slice_bytes
+                send = torch.ones(world * n, dtype=torch.uint8, device="cuda")
+                recv = torch.empty_like(send)
+                for fused in (True, False):
+                    for _ in range(5):
+                        ep.alltoall_packed(send, recv, n, slices_per_peer=kk, fused=fused)
+                    ts = []
+                    for _ in range(25):
+                        e0 = torch.cuda.Event(enable_timing=True)
+                        e1 = torch.cuda.Event(enable_timing=True)
+                        e0.record()
+                        ep.alltoall_packed(send, recv, n, slices_per_peer=kk, fused=fused)
+                        e1.record()
+                        e1.synchronize()
+                        ts.append(e0.elapsed_time(e1))
+                    res[(kk, fused)] = sorted(ts)[len(ts) // 2]
+            for kk in (1, 2, 4, 8):
+                assert res[(kk, True)] <= 1.15 * res[(kk, False)] + 0.005, (kk, res)
+            assert res[(8, True)] < res[(8, False)], res
+            q.put((rank, "ok"))
+            return
         if case == "buckets":
             # gradient-bucket fusion: 5 fp32 "gate gradients" of different
             # sizes, rank-dependent values, pushed in a rank-dependent order;
@@ -133,6 +161,10 @@ def _run(case, world=2):
 
 def test_packed_alltoall_fused_and_unfused():
     _run("a2a")
+
+
+def test_fused_transfer_never_slower():
+    _run("a2a_timing")
 
 
 def test_gradient_buckets_allreduce():
