@@ -116,6 +116,37 @@ def test_layer_ragged_tokens_bf16():
     check_case(E=16, k=2, d=128, dff=256, T=333, cf=2.0, dtype=torch.bfloat16)
 
 
+def _sweep_cases(n=40, seed=2205):
+    """Seeded random shapes inside the layer's contract (bf16: d, d_ff multiples
+    of 128; fp32: multiples of 8): expert counts 1-40, top-1/2, ragged T,
+    capacity factors that drop heavily or not at all, optional gate bias."""
+    rs = np.random.RandomState(seed)
+    out = []
+    for i in range(n):
+        bf = i % 2 == 0
+        E = int(rs.randint(1, 41))
+        k = 1 if E == 1 else int(rs.randint(1, 3))
+        if bf:
+            d, dff = 128 * int(rs.randint(1, 4)), 128 * int(rs.randint(1, 5))
+        else:
+            d, dff = 8 * int(rs.randint(1, 33)), 8 * int(rs.randint(1, 41))
+        T = int(rs.randint(1, 2500))
+        cf = float(np.round(rs.uniform(0.3, 2.5), 2))
+        bias = None
+        if rs.rand() < 0.4:
+            bias = [float(v) for v in rs.normal(0, 1.5, E)]
+        out.append((E, k, d, dff, T, cf, torch.bfloat16 if bf else torch.float32, bias))
+    return out
+
+
+@pytest.mark.parametrize("case", _sweep_cases(), ids=lambda c: "E%d_k%d_d%d_f%d_T%d_cf%s_%s%s" % (
+    c[0], c[1], c[2], c[3], c[4], c[5], "bf16" if c[6] == torch.bfloat16 else "f32",
+    "_bias" if c[7] is not None else ""))
+def test_layer_random_shapes(case):
+    E, k, d, dff, T, cf, dt, bias = case
+    check_case(E=E, k=k, d=d, dff=dff, T=T, cf=cf, dtype=dt, seed=T + E, gate_bias=bias)
+
+
 # ---------------------------------------------------------------- full size --
 def torch_reference(layer, x, dy, rout, d_aux):
     """fp32 torch restatement of Appendix A on the GPU's routing (for sizes the
