@@ -181,3 +181,20 @@ def test_gradient_buckets_allreduce():
 ])
 def test_ep_layer_matches_single_gpu(case):
     _run(case, world=min(torch.cuda.device_count(), 2))
+
+
+def _ep_sweep(n=4, seed=77):
+    import numpy as np
+    rs = np.random.RandomState(seed)
+    out = []
+    for i in range(n):
+        E = 2 * int(rs.randint(1, 24))
+        k = int(rs.randint(1, 3))
+        out.append((E, k, 128 * int(rs.randint(1, 4)), 128 * int(rs.randint(1, 5)),
+                    int(rs.randint(1, 3000)), torch.bfloat16, "p2p" if i % 2 == 0 else "nccl"))
+    return out
+
+
+@pytest.mark.parametrize("case", _ep_sweep())
+def test_ep_layer_random_shapes(case):
+    _run(case, world=2)
