@@ -308,6 +308,7 @@ def main():
     ms = ev0.elapsed_time(ev1)
 
     # ---- separate profiled pass: per-phase CUDA events on the launch stream ----
+    barrier()  # ranks leave the clock sampler at different times: re-align first
     layer.set_profiling(True)
     phase_tot = {}
     for _ in range(args.steps):

@@ -75,6 +75,9 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
   // vector (16-byte) global loads need 4-element aligned rows
   const bool a_vec = (a.lda % 4) == 0 && (reinterpret_cast<uintptr_t>(a.A) & 15) == 0;
   const bool b_vec = (a.ldb % 4) == 0 && (reinterpret_cast<uintptr_t>(a.B) & 15) == 0;
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  const bool c_vec = (a.ldc % 4) == 0 && (a.N % 4) == 0 && al16(a.C) && al16(a.C2) &&
+                     al16(a.aux) && al16(a.bias) && al16(a.gsrc);
 
   const int tx = tid % 16, ty = tid / 16;
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
@@ -219,8 +222,11 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
       }
       __syncthreads();
     }
-    // epilogue: thread rows ty*4 + {0..3}, 64 + ty*4 + {0..3}; columns likewise
+    // epilogue: thread rows ty*4 + {0..3}, 64 + ty*4 + {0..3}; columns
+    // nb*BN + h*64 + tx*4 + {0..3} (h = 0, 1) -- four contiguous columns, so
+    // C / C2 / aux / bias / gathered rows move as float4 when aligned.
     const int bidx = a.kind == 0 ? a.gb[g] : a.gb[tab[g]];
+    float csum[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // DGELU: this thread's column sums
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int m = mb * BM + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
@@ -233,32 +239,92 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
         orow = (long long)bidx * a.M + m;
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int n = nb * BN + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-        if (n >= a.N) continue;
-        float v = (j & 1) ? acc[i][j >> 1].y : acc[i][j >> 1].x;
+      for (int h = 0; h < 2; ++h) {
+        const int n0 = nb * BN + h * 64 + tx * 4;
+        if (n0 >= a.N) continue;
+        float v[4] = {acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y};
         if (a.epi == MOE_EPI_ATOMIC_ADD) {
-          const long long idx = a.transpose_c ? (long long)n * a.ldc + orow : orow * a.ldc + n;
-          atomicAdd(a.C + idx, v);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int n = n0 + c;
+            if (n >= a.N) continue;
+            const long long idx = a.transpose_c ? (long long)n * a.ldc + orow : orow * a.ldc + n;
+            atomicAdd(a.C + idx, v[c]);
+          }
           continue;
         }
-        if (a.bias && a.epi != MOE_EPI_DGELU && a.epi != MOE_EPI_GATHER_ADD)
-          v += a.bias[(long long)bidx * a.N + n];
-        const long long idx = orow * a.ldc + n;
-        if (a.epi == MOE_EPI_GELU) {
-          a.C2[idx] = gelu_grad_f(v);  // stored derivative gelu'(h)
-          v = gelu_f(v);
-        } else if (a.epi == MOE_EPI_DGELU) {
-          v *= a.aux[idx];
-          if (a.colsum) atomicAdd(a.colsum + (long long)bidx * a.N + n, v);
-        } else if (a.epi == MOE_EPI_GATHER_ADD) {
-          for (int r = 0; r < a.gk; ++r) {
-            const int s = a.gidx[orow * a.gk + r];
-            if (s >= 0) v += a.gsrc[(long long)s * a.N + n];
+        const long long idx = orow * a.ldc + n0;
+        if (c_vec && n0 + 3 < a.N) {
+          if (a.bias && a.epi != MOE_EPI_DGELU && a.epi != MOE_EPI_GATHER_ADD) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(a.bias + (long long)bidx * a.N + n0));
+            v[0] += b.x; v[1] += b.y; v[2] += b.z; v[3] += b.w;
           }
+          if (a.epi == MOE_EPI_GELU) {
+            float gr[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) gelu_and_grad_f(v[c], v[c], gr[c]);
+            *reinterpret_cast<float4*>(a.C2 + idx) = make_float4(gr[0], gr[1], gr[2], gr[3]);
+          } else if (a.epi == MOE_EPI_DGELU) {
+            const float4 x4 = __ldg(reinterpret_cast<const float4*>(a.aux + idx));
+            v[0] *= x4.x; v[1] *= x4.y; v[2] *= x4.z; v[3] *= x4.w;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) csum[h * 4 + c] += v[c];
+          } else if (a.epi == MOE_EPI_GATHER_ADD) {
+            for (int r = 0; r < a.gk; ++r) {
+              const int sidx = a.gidx[orow * a.gk + r];
+              if (sidx < 0) continue;
+              const float4 x4 = __ldg(reinterpret_cast<const float4*>(a.gsrc + (long long)sidx * a.N + n0));
+              v[0] += x4.x; v[1] += x4.y; v[2] += x4.z; v[3] += x4.w;
+            }
+          }
+          *reinterpret_cast<float4*>(a.C + idx) = make_float4(v[0], v[1], v[2], v[3]);
+          continue;
         }
-        a.C[idx] = v;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int n = n0 + c;
+          if (n >= a.N) continue;
+          float x = v[c];
+          if (a.bias && a.epi != MOE_EPI_DGELU && a.epi != MOE_EPI_GATHER_ADD)
+            x += a.bias[(long long)bidx * a.N + n];
+          if (a.epi == MOE_EPI_GELU) {
+            float gr;
+            gelu_and_grad_f(x, x, gr);
+            a.C2[idx + c] = gr;  // stored derivative gelu'(h)
+          } else if (a.epi == MOE_EPI_DGELU) {
+            x *= a.aux[idx + c];
+            csum[h * 4 + c] += x;
+          } else if (a.epi == MOE_EPI_GATHER_ADD) {
+            for (int r = 0; r < a.gk; ++r) {
+              const int sidx = a.gidx[orow * a.gk + r];
+              if (sidx >= 0) x += a.gsrc[(long long)sidx * a.N + n];
+            }
+          }
+          a.C[idx + c] = x;
+        }
       }
+    }
+    if (a.epi == MOE_EPI_DGELU && a.colsum) {
+      // db1: column sums of the tile -- the two ty of a warp via shuffle, the
+      // eight warps through shared memory, then one atomic per column and tile
+      // (instead of one per element)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) csum[j] += __shfl_xor_sync(0xffffffffu, csum[j], 16);
+      float* red = &As[0][0][0];  // [8 warps][BN], the K-loop buffers are free here
+      const int wp = tid >> 5;
+      if ((tid & 16) == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) red[wp * BN + (j >> 2) * 64 + tx * 4 + (j & 3)] = csum[j];
+      }
+      __syncthreads();
+      if (tid < BN) {
+        float s = 0.f;
+#pragma unroll
+        for (int w8 = 0; w8 < THREADS / 32; ++w8) s += red[w8 * BN + tid];
+        const int n = nb * BN + tid;
+        if (n < a.N) atomicAdd(a.colsum + (long long)bidx * a.N + n, s);
+      }
+      __syncthreads();  // red aliases As: next tile's stash waits for the readers
     }
   }
 }

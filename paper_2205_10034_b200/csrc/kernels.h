@@ -84,15 +84,30 @@ void combine_backward(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C
                       const float* gate, const int32_t* kept, void* dY, float* dgate,
                       cudaStream_t st);
 
+// fp32 gate GEMMs (gate_f32.cu): logits = x wg^T (+ bg); dwg = dl^T x
+// (zeroes dwg first); dx = dl wg + sum_i dXe[slot_i].  E <= 256.
+void gate_logits_f32(uint64_t T, uint32_t d, uint32_t E, const float* x, const float* wg,
+                     const float* bg, float* logits, cudaStream_t st);
+void gate_wgrad_f32(uint64_t T, uint32_t d, uint32_t E, const float* dl, const float* x,
+                    float* dwg, cudaStream_t st);
+void gate_dx_f32(uint64_t T, uint32_t d, uint32_t E, uint32_t k, const float* dl, const float* wg,
+                 const float* dXe, const int32_t* slot, float* dx, cudaStream_t st);
+
 // dx[t] = dx_gate[t] (fp32, may be null) + sum_i dXe[slot_i].
 void gather_dx(uint64_t T, uint32_t d, uint32_t k, moe_dtype_t dt, const void* dXe,
                const int32_t* slot, const float* dx_gate, void* dx, cudaStream_t st);
 
 // Column sums over the valid rows of each (source, expert) slot group:
 // out[b][n] = sum over groups g with gb[g]==b of sum_{r<m[g]} X[a_row[g]+r][n].
+// With one group per b (bf16), deterministic: row chunks of 512 rows reduce
+// through part_ws (colsum_ws_floats) in chunk order; ticket
+// (colsum_ticket_ints, zeroed once) re-arms itself.
+uint64_t colsum_ws_floats(uint32_t groups, uint32_t N, uint64_t max_rows);
+uint64_t colsum_ticket_ints(uint32_t groups, uint32_t N);
 void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const int32_t* gb,
                   uint32_t num_b, uint32_t N, moe_dtype_t dt, const void* X, float* out,
-                  cudaStream_t st, uint64_t max_rows);
+                  cudaStream_t st, uint64_t max_rows, float* part_ws = nullptr,
+                  int32_t* ticket = nullptr);
 
 // Build the expert GEMM group tables for P source ranks x El local experts from
 // the received kept counts cnt[s][j]: group g = s*El + j, m = cnt, a_row =

@@ -124,6 +124,13 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
     xr = P > 1 ? dalloc_bytes(owned, slot_bytes) : xs;
     cnt_recv = P > 1 ? dalloc<int32_t>(owned, E) : kept;
   }
+  {
+    const uint64_t mr = p2p ? (uint64_t)P * Cs : Cs;
+    cs_part = dalloc<float>(owned, colsum_ws_floats(ngroups, dm, mr));
+    const uint64_t nt = colsum_ticket_ints(ngroups, dm);
+    cs_ticket = dalloc<int32_t>(owned, nt);
+    MOE_CUDA(cudaMemset(cs_ticket, 0, nt * sizeof(int32_t)));
+  }
   gm = dalloc<int32_t>(owned, E);
   ga = dalloc<int32_t>(owned, E);
   gb = dalloc<int32_t>(owned, E);
@@ -248,6 +255,9 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   // K1: logits = x wg^T (+ bg), fp32 out
   if (override_logits) {
     MOE_CUDA(cudaMemcpyAsync(logits, override_logits, T * E * 4, cudaMemcpyDeviceToDevice, st));
+  } else if (T && dt == MOE_DTYPE_F32) {
+    gate_logits_f32(T, dm, E, static_cast<const float*>(x), static_cast<const float*>(w.wg),
+                    desc.has_gate_bias ? static_cast<const float*>(w.bg) : nullptr, logits, st);
   } else if (T) {
     moe_gemm_problem_t p;
     std::memset(&p, 0, sizeof(p));
@@ -387,6 +397,38 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
                  dt == MOE_DTYPE_BF16 ? MOE_DTYPE_BF16 : MOE_DTYPE_F32,
                  dt == MOE_DTYPE_BF16 ? Epad : E, desc.has_gate_bias ? g.dbg : nullptr, st);
   mark("route_bwd", st);
+  // gate weight gradient dwg = dlogits^T x (split-K): needs only local data,
+  // so it runs while the dY rows of the peers are still arriving
+  if (dt == MOE_DTYPE_F32) {
+    gate_wgrad_f32(T, dm, E, dl_f32, static_cast<const float*>(x_saved_ptr), g.dwg, st);
+  } else {
+    MOE_CUDA(cudaMemsetAsync(g.dwg, 0, (uint64_t)E * dm * 4, st));
+  }
+  if (T && dt != MOE_DTYPE_F32) {
+    moe_gemm_problem_t p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = MOE_GEMM_RAGGED_K;
+    p.epilogue = MOE_EPI_ATOMIC_ADD;
+    p.dtype_ab = dt;
+    p.dtype_c = MOE_DTYPE_F32;
+    p.transpose_c = 1;
+    p.groups = nsplit;
+    p.M = dm;
+    p.N = E;
+    p.a_rows = T;
+    p.b_rows = T;
+    p.num_b = 1;
+    p.m = split_m;
+    p.a_row = split_a;
+    p.b = split_b;
+    p.A = x_saved_ptr;
+    p.B = dt == MOE_DTYPE_BF16 ? dl_lp : (const void*)dl_f32;
+    p.ldb = dt == MOE_DTYPE_BF16 ? Epad : E;
+    p.C = g.dwg;
+    p.ldc = dm;
+    grouped_gemm(p, st);
+  }
+  mark("gate_wgrad", st);
   if (p2p) {
     p2p_wait(win, SLOT_DY, ph, st);
     p2p_local_groups(win, gm, ga, gb, dYr, st);  // zero the K-block pad rows of recv_dy
@@ -396,7 +438,8 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   // db2 = column sums of dY, while dY is still warm in L2 (after the weight
   // gradients the L2 is full of dirty fp32 dW lines and every read pays a
   // write-back)
-  group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs);
+  group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs,
+               cs_part, cs_ticket);
   mark("bias_grads", st);
   // Weight-gradient GEMMs (RAGGED_K over the slices of each expert):
   // dW1[j] = sum dH^T X, dW2[j] = sum dY^T A.
@@ -479,8 +522,11 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   mark("wgrad_w2", st);
   if (p2p) p2p_wait(win, SLOT_DX, ph, st);
   // gate dgrad with the combine backward folded into its epilogue:
-  // dx[t] = dlogits[t] wg + sum_i dXe[slot_i]; dwg = dlogits^T x (split-K)
-  if (T) {
+  // dx[t] = dlogits[t] wg + sum_i dXe[slot_i]
+  if (T && dt == MOE_DTYPE_F32) {
+    gate_dx_f32(T, dm, E, k, dl_f32, static_cast<const float*>(w.wg),
+                static_cast<const float*>(dXh), slot, static_cast<float*>(dx), st);
+  } else if (T) {
     moe_gemm_problem_t p;
     std::memset(&p, 0, sizeof(p));
     p.kind = MOE_GEMM_RAGGED_M;
@@ -508,32 +554,6 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("gate_dgrad_gather_dx", st);
-  MOE_CUDA(cudaMemsetAsync(g.dwg, 0, (uint64_t)E * dm * 4, st));
-  if (T) {
-    moe_gemm_problem_t p;
-    std::memset(&p, 0, sizeof(p));
-    p.kind = MOE_GEMM_RAGGED_K;
-    p.epilogue = MOE_EPI_ATOMIC_ADD;
-    p.dtype_ab = dt;
-    p.dtype_c = MOE_DTYPE_F32;
-    p.transpose_c = 1;
-    p.groups = nsplit;
-    p.M = dm;
-    p.N = E;
-    p.a_rows = T;
-    p.b_rows = T;
-    p.num_b = 1;
-    p.m = split_m;
-    p.a_row = split_a;
-    p.b = split_b;
-    p.A = x_saved_ptr;
-    p.B = dt == MOE_DTYPE_BF16 ? dl_lp : (const void*)dl_f32;
-    p.ldb = dt == MOE_DTYPE_BF16 ? Epad : E;
-    p.C = g.dwg;
-    p.ldc = dm;
-    grouped_gemm(p, st);
-  }
-  mark("gate_wgrad", st);
   if (p2p) {
     // replicated gate gradients: one-shot all-reduce over the peer windows
     p2p_allreduce_f32(win, g.dwg, (uint64_t)E * dm, desc.has_gate_bias ? g.dbg : nullptr,

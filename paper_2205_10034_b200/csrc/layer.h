@@ -61,6 +61,8 @@ struct Layer {
   int32_t* cnt_recv = nullptr;
   int32_t *gm = nullptr, *ga = nullptr, *gb = nullptr, *gmk = nullptr, *gak = nullptr,
           *gbk = nullptr;
+  float* cs_part = nullptr;      // db2 chunk partials (group_colsum)
+  int32_t* cs_ticket = nullptr;  // db2 chunk tickets, self re-arming
   void *Gp = nullptr, *Aact = nullptr, *Yl = nullptr, *Yh = nullptr;
   // backward buffers
   float* dgate = nullptr;

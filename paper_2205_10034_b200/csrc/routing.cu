@@ -710,19 +710,31 @@ __global__ void colsum_bf16x8_kernel(const int32_t* __restrict__ gm, const int32
 // columns each), 8 rows in flight per thread — and reduces the row lanes in a
 // fixed order through shared memory: deterministic, no atomics, no memset.
 constexpr int CS_LANES = 16;
+// One block per (group, row chunk of CS_CHUNK rows, 256 columns): chunk
+// partials go to a workspace and the last chunk block of a (group, column
+// block) to finish -- an acq_rel ticket -- sums them in chunk order, so db2 is
+// deterministic and a heavily loaded expert (skewed routing) is spread over
+// many blocks instead of serialising on one.
+constexpr int CS_CHUNK = 512;
+
 __global__ void __launch_bounds__(CS_LANES * 32) colsum_group_bf16_kernel(
     const int32_t* __restrict__ gm, const int32_t* __restrict__ ga, const int32_t* __restrict__ gb,
-    int N, const __nv_bfloat16* __restrict__ X, float* __restrict__ out) {
+    int N, int maxch, const __nv_bfloat16* __restrict__ X, float* __restrict__ out,
+    float* __restrict__ part_ws, int32_t* __restrict__ ticket) {
   __shared__ float part[CS_LANES][256 + 8];
-  const int g = blockIdx.x;
+  __shared__ int last;
+  const int g = blockIdx.x / maxch, ch = blockIdx.x % maxch;
   const int rows = gm[g];
+  const int nch = max(1, (rows + CS_CHUNK - 1) / CS_CHUNK);
+  if (ch >= nch) return;
+  const int r_end = min(rows, (ch + 1) * CS_CHUNK);
   const int cl = threadIdx.x & 31, rl = threadIdx.x >> 5;
   const int n = blockIdx.y * 256 + cl * 8;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (n < N) {
     const __nv_bfloat16* base = X + (uint64_t)ga[g] * N + n;
-    int r = rl;
-    for (; r + 7 * CS_LANES < rows; r += 8 * CS_LANES) {
+    int r = ch * CS_CHUNK + rl;
+    for (; r + 7 * CS_LANES < r_end; r += 8 * CS_LANES) {
       uint4 v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u)
@@ -738,7 +750,7 @@ __global__ void __launch_bounds__(CS_LANES * 32) colsum_group_bf16_kernel(
         }
       }
     }
-    for (; r < rows; r += CS_LANES) {
+    for (; r < r_end; r += CS_LANES) {
       const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (uint64_t)r * N));
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
@@ -752,12 +764,35 @@ __global__ void __launch_bounds__(CS_LANES * 32) colsum_group_bf16_kernel(
 #pragma unroll
   for (int q = 0; q < 8; ++q) part[rl][cl * 8 + q] = acc[q];
   __syncthreads();
+  const int col = blockIdx.y * 256 + threadIdx.x;
+  float sum = 0.f;
   if (threadIdx.x < 256) {
-    const int col = blockIdx.y * 256 + threadIdx.x;
-    float sum = 0.f;
 #pragma unroll
     for (int l = 0; l < CS_LANES; ++l) sum += part[l][threadIdx.x];
-    if (col < N) out[(uint64_t)gb[g] * N + col] = sum;
+  }
+  if (nch == 1) {
+    if (threadIdx.x < 256 && col < N) out[(uint64_t)gb[g] * N + col] = sum;
+    return;
+  }
+  float* const mine = part_ws + ((uint64_t)g * maxch + ch) * N;
+  if (threadIdx.x < 256 && col < N) mine[col] = sum;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int32_t* t = ticket + (uint64_t)g * gridDim.y + blockIdx.y;
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(t) : "memory");
+    last = old == nch - 1;
+    if (last) *t = 0;  // every chunk block has arrived: re-arm for the next launch
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 256 && col < N) {
+    const float* p = part_ws + (uint64_t)g * maxch * N + col;
+    float s = 0.f;
+    for (int c = 0; c < nch; ++c) s += __ldcg(p + (uint64_t)c * N);
+    out[(uint64_t)gb[g] * N + col] = s;
   }
 }
 
@@ -880,13 +915,22 @@ void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, con
   count_launch();
 }
 
+uint64_t colsum_ws_floats(uint32_t groups, uint32_t N, uint64_t max_rows) {
+  return (uint64_t)groups * std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)CS_CHUNK)) * N;
+}
+uint64_t colsum_ticket_ints(uint32_t groups, uint32_t N) {
+  return (uint64_t)groups * ceil_div((uint64_t)N, (uint64_t)256);
+}
+
 void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const int32_t* gb,
                   uint32_t num_b, uint32_t N, moe_dtype_t dt, const void* X, float* out,
-                  cudaStream_t st, uint64_t max_rows) {
-  if (dt == MOE_DTYPE_BF16 && N % 8 == 0 && groups == num_b) {
+                  cudaStream_t st, uint64_t max_rows, float* part_ws, int32_t* ticket) {
+  if (dt == MOE_DTYPE_BF16 && N % 8 == 0 && groups == num_b && part_ws && ticket) {
     // one group per expert (N = 1 and the P2P exchange): gb is a permutation
-    colsum_group_bf16_kernel<<<dim3(groups, (unsigned)ceil_div(N, 256)), CS_LANES * 32, 0, st>>>(
-        gm, ga, gb, (int)N, (const __nv_bfloat16*)X, out);
+    const int maxch = (int)std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)CS_CHUNK));
+    colsum_group_bf16_kernel<<<dim3(groups * maxch, (unsigned)ceil_div(N, 256)), CS_LANES * 32, 0,
+                               st>>>(gm, ga, gb, (int)N, maxch, (const __nv_bfloat16*)X, out,
+                                     part_ws, ticket);
     MOE_LAUNCH_CHECK("colsum_group_bf16_kernel");
     count_launch();
     return;

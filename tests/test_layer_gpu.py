@@ -253,6 +253,8 @@ def test_gradient_buckets_single_rank_scale():
     (8, 1, 1, 1.25, torch.bfloat16),      # one token
     (8, 2, 300, 0.05, torch.bfloat16),    # tiny capacity: most assignments dropped
     (4, 2, 77, 2.0, torch.float32),       # fp32, ragged T
+    (256, 2, 700, 1.5, torch.float32),    # fp32 at the expert limit (gate kernels' widest case)
+    (61, 1, 333, 1.0, torch.float32),     # fp32, odd expert count (partial expert chunks)
 ])
 def test_layer_edge_cases(E, k, T, cf, dtype):
     """Edge cases of Appendix A: single expert, E = k, one token, heavy drops,
