@@ -17,6 +17,9 @@ namespace simt {
 // while the current one is multiplied.
 constexpr int BM = 128, BN = 128, BK = 16, THREADS = 256, MAX_GROUPS = 1024;
 constexpr int PAD = 4;
+#ifndef SIMT_MINB
+#define SIMT_MINB 2  // 2 CTAs per SM: A/B on c1 +2.7% over 1 (small epilogue-only spills)
+#endif
 
 struct Args {
   int kind, epi, groups, M, N, K, b_mn, transpose_c;
@@ -38,7 +41,10 @@ struct Slice {
   float4 a[2], b[2];
 };
 
-__global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
+// Specialised per (kind, B layout, epilogue) so the bounds / layout branches
+// fold at compile time (fewer live registers in the K loop).
+template <int KIND, int BMN, int EPI>
+__global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Args a) {
   __shared__ __align__(16) float As[2][BK][BM + PAD];
   __shared__ __align__(16) float Bs[2][BK][BN + PAD];
   __shared__ int tab[MAX_GROUPS + 1];
@@ -49,16 +55,16 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
   const int nbm_k = (a.M + BM - 1) / BM;  // RAGGED_K tiles along M
 
   for (int g = tid; g < G; g += THREADS) {
-    if (a.kind == 0) {
+    if (KIND == 0) {
       cnt[g] = ((a.gm[g] + BM - 1) / BM) * nbn;
     } else {
-      const bool start = a.epi == MOE_EPI_ATOMIC_ADD || g == 0 || a.gb[g] != a.gb[g - 1];
+      const bool start = EPI == MOE_EPI_ATOMIC_ADD || g == 0 || a.gb[g] != a.gb[g - 1];
       cnt[g] = start ? 1 : 0;
     }
   }
   __syncthreads();
   if (tid == 0) {
-    if (a.kind == 0) {
+    if (KIND == 0) {
       int run = 0;
       for (int g = 0; g < G; ++g) { tab[g] = run; run += cnt[g]; }
       tab[G] = run;
@@ -71,7 +77,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
     }
   }
   __syncthreads();
-  const int total = a.kind == 0 ? tab[G] : cnt[0] * nbm_k * nbn;
+  const int total = KIND == 0 ? tab[G] : cnt[0] * nbm_k * nbn;
   // vector (16-byte) global loads need 4-element aligned rows
   const bool a_vec = (a.lda % 4) == 0 && (reinterpret_cast<uintptr_t>(a.A) & 15) == 0;
   const bool b_vec = (a.ldb % 4) == 0 && (reinterpret_cast<uintptr_t>(a.B) & 15) == 0;
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
   const int tx = tid % 16, ty = tid / 16;
   for (int w = blockIdx.x; w < total; w += gridDim.x) {
     int g, mb, nb;
-    if (a.kind == 0) {
+    if (KIND == 0) {
       int lo = 0, hi = G;
       while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
@@ -105,25 +111,25 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
       for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
     // K iteration: RAGGED_M -> one range [0,K) on row base ga[g]+mb*BM;
     // RAGGED_K -> rows of every group of segment g.
-    const int q0 = a.kind == 0 ? g : tab[g];
-    const int q1 = a.kind == 0 ? g + 1 : tab[g + 1];
+    const int q0 = KIND == 0 ? g : tab[g];
+    const int q1 = KIND == 0 ? g + 1 : tab[g + 1];
     for (int q = q0; q < q1; ++q) {
-      const int klen = a.kind == 0 ? a.K : a.gm[q];
-      const int mrows = a.kind == 0 ? a.gm[q] : a.M;
+      const int klen = KIND == 0 ? a.K : a.gm[q];
+      const int mrows = KIND == 0 ? a.gm[q] : a.M;
       const long long r0 = a.ga[q];
-      const long long bbase = a.kind == 0 ? (long long)a.gb[q] * (a.b_mn ? a.K : a.N) : r0;
+      const long long bbase = KIND == 0 ? (long long)a.gb[q] * (BMN ? a.K : a.N) : r0;
       // element (m, k) of A / (n, k) of B with bounds (0 outside)
       auto ldA = [&](int m, int k) -> float {
         if (m >= mrows || k >= klen) return 0.f;
-        return a.kind == 0 ? a.A[(r0 + m) * a.lda + k] : a.A[(r0 + k) * a.lda + m];
+        return KIND == 0 ? a.A[(r0 + m) * a.lda + k] : a.A[(r0 + k) * a.lda + m];
       };
       auto ldB = [&](int n, int k) -> float {
         if (n >= a.N || k >= klen) return 0.f;
-        if (a.kind == 0 && !a.b_mn) {
+        if (KIND == 0 && !BMN) {
           const long long br = bbase + n;
           return br < a.b_rows ? a.B[br * a.ldb + k] : 0.f;
         }
-        if (a.kind == 0) {
+        if (KIND == 0) {
           const long long br = bbase + k;
           return br < a.b_rows ? a.B[br * a.ldb + n] : 0.f;
         }
@@ -136,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int f = tid + THREADS * i;
-          if (a.kind == 0) {  // A: [m][k]
+          if (KIND == 0) {  // A: [m][k]
             const int mm = f >> 2, k = k0 + (f & 3) * 4, m = mb * BM + mm;
             if (a_vec && m < mrows && k + 3 < klen)
               sl.a[i] = __ldg(reinterpret_cast<const float4*>(a.A + (r0 + m) * a.lda + k));
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
             else
               sl.a[i] = make_float4(ldA(m, k), ldA(m + 1, k), ldA(m + 2, k), ldA(m + 3, k));
           }
-          if (a.kind == 0 && !a.b_mn) {  // B: [n][k]
+          if (KIND == 0 && !BMN) {  // B: [n][k]
             const int nn = f >> 2, k = k0 + (f & 3) * 4, n = nb * BN + nn;
             const long long br = bbase + n;
             if (b_vec && n < a.N && k + 3 < klen && br < a.b_rows)
@@ -159,7 +165,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
           } else {  // B: [k][n]
             const int kk = f >> 5, n = nb * BN + (f & 31) * 4, k = k0 + kk;
             const long long br = bbase + k;
-            if (b_vec && n + 3 < a.N && k < klen && (a.kind != 0 || br < a.b_rows))
+            if (b_vec && n + 3 < a.N && k < klen && (KIND != 0 || br < a.b_rows))
               sl.b[i] = __ldg(reinterpret_cast<const float4*>(a.B + br * a.ldb + n));
             else
               sl.b[i] = make_float4(ldB(n, k), ldB(n + 1, k), ldB(n + 2, k), ldB(n + 3, k));
@@ -170,7 +176,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int f = tid + THREADS * i;
-          if (a.kind == 0) {
+          if (KIND == 0) {
             const int mm = f >> 2, kq = (f & 3) * 4;
             As[buf][kq][mm] = sl.a[i].x;
             As[buf][kq + 1][mm] = sl.a[i].y;
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
           } else {
             *reinterpret_cast<float4*>(&As[buf][f >> 5][(f & 31) * 4]) = sl.a[i];
           }
-          if (a.kind == 0 && !a.b_mn) {
+          if (KIND == 0 && !BMN) {
             const int nn = f >> 2, kq = (f & 3) * 4;
             Bs[buf][kq][nn] = sl.b[i].x;
             Bs[buf][kq + 1][nn] = sl.b[i].y;
@@ -225,13 +231,13 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
     // epilogue: thread rows ty*4 + {0..3}, 64 + ty*4 + {0..3}; columns
     // nb*BN + h*64 + tx*4 + {0..3} (h = 0, 1) -- four contiguous columns, so
     // C / C2 / aux / bias / gathered rows move as float4 when aligned.
-    const int bidx = a.kind == 0 ? a.gb[g] : a.gb[tab[g]];
+    const int bidx = KIND == 0 ? a.gb[g] : a.gb[tab[g]];
     float csum[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // DGELU: this thread's column sums
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int m = mb * BM + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
       long long orow;
-      if (a.kind == 0) {
+      if (KIND == 0) {
         if (m >= a.gm[g]) continue;
         orow = (long long)a.gc[g] + m;
       } else {
@@ -243,7 +249,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
         const int n0 = nb * BN + h * 64 + tx * 4;
         if (n0 >= a.N) continue;
         float v[4] = {acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y};
-        if (a.epi == MOE_EPI_ATOMIC_ADD) {
+        if (EPI == MOE_EPI_ATOMIC_ADD) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const int n = n0 + c;
@@ -255,21 +261,21 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
         }
         const long long idx = orow * a.ldc + n0;
         if (c_vec && n0 + 3 < a.N) {
-          if (a.bias && a.epi != MOE_EPI_DGELU && a.epi != MOE_EPI_GATHER_ADD) {
+          if (a.bias && EPI != MOE_EPI_DGELU && EPI != MOE_EPI_GATHER_ADD) {
             const float4 b = __ldg(reinterpret_cast<const float4*>(a.bias + (long long)bidx * a.N + n0));
             v[0] += b.x; v[1] += b.y; v[2] += b.z; v[3] += b.w;
           }
-          if (a.epi == MOE_EPI_GELU) {
+          if (EPI == MOE_EPI_GELU) {
             float gr[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) gelu_and_grad_f(v[c], v[c], gr[c]);
             *reinterpret_cast<float4*>(a.C2 + idx) = make_float4(gr[0], gr[1], gr[2], gr[3]);
-          } else if (a.epi == MOE_EPI_DGELU) {
+          } else if (EPI == MOE_EPI_DGELU) {
             const float4 x4 = __ldg(reinterpret_cast<const float4*>(a.aux + idx));
             v[0] *= x4.x; v[1] *= x4.y; v[2] *= x4.z; v[3] *= x4.w;
 #pragma unroll
             for (int c = 0; c < 4; ++c) csum[h * 4 + c] += v[c];
-          } else if (a.epi == MOE_EPI_GATHER_ADD) {
+          } else if (EPI == MOE_EPI_GATHER_ADD) {
             for (int r = 0; r < a.gk; ++r) {
               const int sidx = a.gidx[orow * a.gk + r];
               if (sidx < 0) continue;
@@ -285,16 +291,16 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
           const int n = n0 + c;
           if (n >= a.N) continue;
           float x = v[c];
-          if (a.bias && a.epi != MOE_EPI_DGELU && a.epi != MOE_EPI_GATHER_ADD)
+          if (a.bias && EPI != MOE_EPI_DGELU && EPI != MOE_EPI_GATHER_ADD)
             x += a.bias[(long long)bidx * a.N + n];
-          if (a.epi == MOE_EPI_GELU) {
+          if (EPI == MOE_EPI_GELU) {
             float gr;
             gelu_and_grad_f(x, x, gr);
             a.C2[idx + c] = gr;  // stored derivative gelu'(h)
-          } else if (a.epi == MOE_EPI_DGELU) {
+          } else if (EPI == MOE_EPI_DGELU) {
             x *= a.aux[idx + c];
             csum[h * 4 + c] += x;
-          } else if (a.epi == MOE_EPI_GATHER_ADD) {
+          } else if (EPI == MOE_EPI_GATHER_ADD) {
             for (int r = 0; r < a.gk; ++r) {
               const int sidx = a.gidx[orow * a.gk + r];
               if (sidx >= 0) x += a.gsrc[(long long)sidx * a.N + n];
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(THREADS, 1) simt_gemm_kernel(const Args a) {
         }
       }
     }
-    if (a.epi == MOE_EPI_DGELU && a.colsum) {
+    if (EPI == MOE_EPI_DGELU && a.colsum) {
       // db1: column sums of the tile -- the two ty of a warp via shuffle, the
       // eight warps through shared memory, then one atomic per column and tile
       // (instead of one per element)
@@ -371,7 +377,31 @@ void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
     a.ldb = p.ldb ? p.ldb : p.N;
   }
   const int grid = num_sms() * 4;
-  simt_gemm_kernel<<<grid, THREADS, 0, st>>>(a);
+  auto go = [&](auto kern) { kern<<<grid, THREADS, 0, st>>>(a); };
+  if (p.kind == MOE_GEMM_RAGGED_K) {
+    if (p.epilogue == MOE_EPI_ATOMIC_ADD) go(simt_gemm_kernel<1, 0, MOE_EPI_ATOMIC_ADD>);
+    else go(simt_gemm_kernel<1, 0, MOE_EPI_STORE>);
+  } else {
+    const bool bmn = p.b_mn_major != 0;
+    switch (p.epilogue) {
+      case MOE_EPI_GELU:
+        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_GELU>) : go(simt_gemm_kernel<0, 0, MOE_EPI_GELU>);
+        break;
+      case MOE_EPI_DGELU:
+        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_DGELU>) : go(simt_gemm_kernel<0, 0, MOE_EPI_DGELU>);
+        break;
+      case MOE_EPI_GATHER_ADD:
+        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_GATHER_ADD>)
+            : go(simt_gemm_kernel<0, 0, MOE_EPI_GATHER_ADD>);
+        break;
+      case MOE_EPI_ATOMIC_ADD:
+        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_ATOMIC_ADD>)
+            : go(simt_gemm_kernel<0, 0, MOE_EPI_ATOMIC_ADD>);
+        break;
+      default:
+        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_STORE>) : go(simt_gemm_kernel<0, 0, MOE_EPI_STORE>);
+    }
+  }
   MOE_LAUNCH_CHECK("simt_gemm_kernel");
   count_launch();
 }
