@@ -4,6 +4,8 @@
 // out TF32 tensor cores; this kernel keeps fp32 operands and fp32 FFMA
 // accumulation with the same group tables and epilogues as the tcgen05 kernel
 // (gemm_tc.cu), so the layer orchestration is dtype-agnostic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -43,8 +45,12 @@ struct Slice {
 
 // Specialised per (kind, B layout, epilogue) so the bounds / layout branches
 // fold at compile time (fewer live registers in the K loop).
-template <int KIND, int BMN, int EPI>
+// BNT = 128 (8 x 8 per thread) or 64 (8 x 4 per thread: twice the tiles, for
+// the narrow GEMMs whose 128 x 128 tiles leave SMs idle in the last wave).
+template <int KIND, int BMN, int EPI, int BNT>
 __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Args a) {
+  constexpr int BN = BNT, NH = BNT / 64;  // column halves of 64 per thread tile
+  constexpr int C4 = BN / 4;              // float4 per B row of the slice ([k][n])
   __shared__ __align__(16) float As[2][BK][BM + PAD];
   __shared__ __align__(16) float Bs[2][BK][BN + PAD];
   __shared__ int tab[MAX_GROUPS + 1];
@@ -104,11 +110,11 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
       mb = (w % per) / nbn;
       nb = (w % per) % nbn;
     }
-    float2 acc[8][4];
+    float2 acc[8][2 * NH];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = make_float2(0.f, 0.f);
+      for (int j = 0; j < 2 * NH; ++j) acc[i][j] = make_float2(0.f, 0.f);
     // K iteration: RAGGED_M -> one range [0,K) on row base ga[g]+mb*BM;
     // RAGGED_K -> rows of every group of segment g.
     const int q0 = KIND == 0 ? g : tab[g];
@@ -155,6 +161,7 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
             else
               sl.a[i] = make_float4(ldA(m, k), ldA(m + 1, k), ldA(m + 2, k), ldA(m + 3, k));
           }
+          if (i >= NH) continue;  // B slice: BN * BK / 4 float4 = NH per thread
           if (KIND == 0 && !BMN) {  // B: [n][k]
             const int nn = f >> 2, k = k0 + (f & 3) * 4, n = nb * BN + nn;
             const long long br = bbase + n;
@@ -163,7 +170,7 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
             else
               sl.b[i] = make_float4(ldB(n, k), ldB(n, k + 1), ldB(n, k + 2), ldB(n, k + 3));
           } else {  // B: [k][n]
-            const int kk = f >> 5, n = nb * BN + (f & 31) * 4, k = k0 + kk;
+            const int kk = f / C4, n = nb * BN + (f % C4) * 4, k = k0 + kk;
             const long long br = bbase + k;
             if (b_vec && n + 3 < a.N && k < klen && (KIND != 0 || br < a.b_rows))
               sl.b[i] = __ldg(reinterpret_cast<const float4*>(a.B + br * a.ldb + n));
@@ -185,6 +192,7 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
           } else {
             *reinterpret_cast<float4*>(&As[buf][f >> 5][(f & 31) * 4]) = sl.a[i];
           }
+          if (i >= NH) continue;
           if (KIND == 0 && !BMN) {
             const int nn = f >> 2, kq = (f & 3) * 4;
             Bs[buf][kq][nn] = sl.b[i].x;
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
             Bs[buf][kq + 2][nn] = sl.b[i].z;
             Bs[buf][kq + 3][nn] = sl.b[i].w;
           } else {
-            *reinterpret_cast<float4*>(&Bs[buf][f >> 5][(f & 31) * 4]) = sl.b[i];
+            *reinterpret_cast<float4*>(&Bs[buf][f / C4][(f % C4) * 4]) = sl.b[i];
           }
         }
       };
@@ -209,15 +217,18 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
         for (int kk = 0; kk < BK; ++kk) {
           const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
           const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
-          const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
-          const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
           const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-          const float2 bv[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w),
-                                make_float2(b1.x, b1.y), make_float2(b1.z, b1.w)};
+          float2 bv[2 * NH];
+#pragma unroll
+          for (int h = 0; h < NH; ++h) {
+            const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 * h + tx * 4]);
+            bv[2 * h] = make_float2(b.x, b.y);
+            bv[2 * h + 1] = make_float2(b.z, b.w);
+          }
 #pragma unroll
           for (int i = 0; i < 8; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < 2 * NH; ++j)
               acc[i][j] = __ffma2_rn(make_float2(av[i], av[i]), bv[j], acc[i][j]);
         }
         if (more) {
@@ -232,7 +243,9 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
     // nb*BN + h*64 + tx*4 + {0..3} (h = 0, 1) -- four contiguous columns, so
     // C / C2 / aux / bias / gathered rows move as float4 when aligned.
     const int bidx = KIND == 0 ? a.gb[g] : a.gb[tab[g]];
-    float csum[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // DGELU: this thread's column sums
+    float csum[4 * NH];  // DGELU: this thread's column sums
+#pragma unroll
+    for (int j = 0; j < 4 * NH; ++j) csum[j] = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int m = mb * BM + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
@@ -245,7 +258,7 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
         orow = (long long)bidx * a.M + m;
       }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < NH; ++h) {
         const int n0 = nb * BN + h * 64 + tx * 4;
         if (n0 >= a.N) continue;
         float v[4] = {acc[i][2 * h].x, acc[i][2 * h].y, acc[i][2 * h + 1].x, acc[i][2 * h + 1].y};
@@ -315,12 +328,12 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
       // eight warps through shared memory, then one atomic per column and tile
       // (instead of one per element)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) csum[j] += __shfl_xor_sync(0xffffffffu, csum[j], 16);
+      for (int j = 0; j < 4 * NH; ++j) csum[j] += __shfl_xor_sync(0xffffffffu, csum[j], 16);
       float* red = &As[0][0][0];  // [8 warps][BN], the K-loop buffers are free here
       const int wp = tid >> 5;
       if ((tid & 16) == 0) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) red[wp * BN + (j >> 2) * 64 + tx * 4 + (j & 3)] = csum[j];
+        for (int j = 0; j < 4 * NH; ++j) red[wp * BN + (j >> 2) * 64 + tx * 4 + (j & 3)] = csum[j];
       }
       __syncthreads();
       if (tid < BN) {
@@ -335,6 +348,22 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
   }
 }
 
+}  // namespace simt
+
+namespace simt {
+// Host-side tile-count estimate (row counts live on the device: the A row
+// capacity stands in for them). MOE_SIMT_BN64=0/1 forces a width (A/B runs).
+bool simt_use_bn64(const moe_gemm_problem_t& p) {
+  static const char* env = std::getenv("MOE_SIMT_BN64");
+  if (env && env[0] == '0') return false;
+  if (env && env[0] == '1') return true;
+  // measured on c1 (A/B): the weight-gradient GEMMs gain 6%, the ragged-M
+  // ones do not (dgrad-ffn1 loses 14%), so only RAGGED_K switches
+  if (p.kind != MOE_GEMM_RAGGED_K) return false;
+  const uint64_t tiles =
+      ceil_div(p.M, (uint64_t)BM) * ceil_div(p.N, (uint64_t)BN) * std::max<uint64_t>(1, p.num_b);
+  return tiles < 4ull * (uint64_t)num_sms();
+}
 }  // namespace simt
 
 void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
@@ -377,29 +406,35 @@ void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
     a.ldb = p.ldb ? p.ldb : p.N;
   }
   const int grid = num_sms() * 4;
-  auto go = [&](auto kern) { kern<<<grid, THREADS, 0, st>>>(a); };
+  // 64-wide column tiles when 128-wide ones would leave SMs idle in the last
+  // wave (fewer than ~4 tiles per SM): c1's weight-gradient GEMMs
+  const bool narrow = simt_use_bn64(p);
+  auto go2 = [&](auto k128, auto k64) {
+    if (narrow) k64<<<grid, THREADS, 0, st>>>(a);
+    else k128<<<grid, THREADS, 0, st>>>(a);
+  };
   if (p.kind == MOE_GEMM_RAGGED_K) {
-    if (p.epilogue == MOE_EPI_ATOMIC_ADD) go(simt_gemm_kernel<1, 0, MOE_EPI_ATOMIC_ADD>);
-    else go(simt_gemm_kernel<1, 0, MOE_EPI_STORE>);
+    if (p.epilogue == MOE_EPI_ATOMIC_ADD) go2(simt_gemm_kernel<1, 0, MOE_EPI_ATOMIC_ADD, 128>, simt_gemm_kernel<1, 0, MOE_EPI_ATOMIC_ADD, 64>);
+    else go2(simt_gemm_kernel<1, 0, MOE_EPI_STORE, 128>, simt_gemm_kernel<1, 0, MOE_EPI_STORE, 64>);
   } else {
     const bool bmn = p.b_mn_major != 0;
     switch (p.epilogue) {
       case MOE_EPI_GELU:
-        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_GELU>) : go(simt_gemm_kernel<0, 0, MOE_EPI_GELU>);
+        bmn ? go2(simt_gemm_kernel<0, 1, MOE_EPI_GELU, 128>, simt_gemm_kernel<0, 1, MOE_EPI_GELU, 64>) : go2(simt_gemm_kernel<0, 0, MOE_EPI_GELU, 128>, simt_gemm_kernel<0, 0, MOE_EPI_GELU, 64>);
         break;
       case MOE_EPI_DGELU:
-        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_DGELU>) : go(simt_gemm_kernel<0, 0, MOE_EPI_DGELU>);
+        bmn ? go2(simt_gemm_kernel<0, 1, MOE_EPI_DGELU, 128>, simt_gemm_kernel<0, 1, MOE_EPI_DGELU, 64>) : go2(simt_gemm_kernel<0, 0, MOE_EPI_DGELU, 128>, simt_gemm_kernel<0, 0, MOE_EPI_DGELU, 64>);
         break;
       case MOE_EPI_GATHER_ADD:
-        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_GATHER_ADD>)
-            : go(simt_gemm_kernel<0, 0, MOE_EPI_GATHER_ADD>);
+        bmn ? go2(simt_gemm_kernel<0, 1, MOE_EPI_GATHER_ADD, 128>, simt_gemm_kernel<0, 1, MOE_EPI_GATHER_ADD, 64>)
+            : go2(simt_gemm_kernel<0, 0, MOE_EPI_GATHER_ADD, 128>, simt_gemm_kernel<0, 0, MOE_EPI_GATHER_ADD, 64>);
         break;
       case MOE_EPI_ATOMIC_ADD:
-        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_ATOMIC_ADD>)
-            : go(simt_gemm_kernel<0, 0, MOE_EPI_ATOMIC_ADD>);
+        bmn ? go2(simt_gemm_kernel<0, 1, MOE_EPI_ATOMIC_ADD, 128>, simt_gemm_kernel<0, 1, MOE_EPI_ATOMIC_ADD, 64>)
+            : go2(simt_gemm_kernel<0, 0, MOE_EPI_ATOMIC_ADD, 128>, simt_gemm_kernel<0, 0, MOE_EPI_ATOMIC_ADD, 64>);
         break;
       default:
-        bmn ? go(simt_gemm_kernel<0, 1, MOE_EPI_STORE>) : go(simt_gemm_kernel<0, 0, MOE_EPI_STORE>);
+        bmn ? go2(simt_gemm_kernel<0, 1, MOE_EPI_STORE, 128>, simt_gemm_kernel<0, 1, MOE_EPI_STORE, 64>) : go2(simt_gemm_kernel<0, 0, MOE_EPI_STORE, 128>, simt_gemm_kernel<0, 0, MOE_EPI_STORE, 64>);
     }
   }
   MOE_LAUNCH_CHECK("simt_gemm_kernel");
