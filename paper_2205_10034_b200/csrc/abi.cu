@@ -1,6 +1,7 @@
 // extern "C" boundary (include/moe_b200.h): converts moe::Error / C++
 // exceptions into moe_status_t + a thread-local "<field>: <reason>" message,
 // mirroring the reference's exception taxonomy.
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <new>
@@ -18,6 +19,13 @@
 namespace moe {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MOE_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 }  // namespace moe
 
 namespace {

@@ -26,6 +26,8 @@ __global__ void __launch_bounds__(GT) gate_logits_f32_kernel(uint64_t T, int d, 
                                                              const float* __restrict__ wg,
                                                              const float* __restrict__ bg,
                                                              float* __restrict__ logits) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const uint64_t t = (uint64_t)blockIdx.x * (GT / 32) + (threadIdx.x >> 5);
   if (t >= T) return;
@@ -72,6 +74,8 @@ __global__ void __launch_bounds__(GT) gate_wgrad_f32_kernel(uint64_t T, int d, i
                                                             const float* __restrict__ dl,
                                                             const float* __restrict__ x,
                                                             float* __restrict__ dwg) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float dls[];  // [TOKC][E]
   const uint64_t t0 = (uint64_t)blockIdx.x * TOKC;
   const int ntok = (int)(T - t0 < (uint64_t)TOKC ? T - t0 : (uint64_t)TOKC);
@@ -105,6 +109,8 @@ __global__ void __launch_bounds__(GT) gate_dx_f32_kernel(uint64_t T, int d, int 
                                                          const float* __restrict__ dXe,
                                                          const int32_t* __restrict__ slot,
                                                          float* __restrict__ dx) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   float* wsm = sm;            // [E][64]
   float* dls = sm + E * 64;   // [DX_TOK][E + 1]
@@ -153,9 +159,9 @@ void gate_logits_f32(uint64_t T, uint32_t d, uint32_t E, const float* x, const f
                    (reinterpret_cast<uintptr_t>(wg) & 15) == 0;
   const unsigned grid = (unsigned)ceil_div(T, (uint64_t)(GT / 32));
   if (vec)
-    gate_logits_f32_kernel<true><<<grid, GT, 0, st>>>(T, (int)d, (int)E, x, wg, bg, logits);
+    launch_pdl(gate_logits_f32_kernel<true>, grid, GT, 0, st, T, (int)d, (int)E, x, wg, bg, logits);
   else
-    gate_logits_f32_kernel<false><<<grid, GT, 0, st>>>(T, (int)d, (int)E, x, wg, bg, logits);
+    launch_pdl(gate_logits_f32_kernel<false>, grid, GT, 0, st, T, (int)d, (int)E, x, wg, bg, logits);
   MOE_LAUNCH_CHECK("gate_logits_f32_kernel");
   count_launch();
 }
@@ -170,7 +176,7 @@ void gate_wgrad_f32(uint64_t T, uint32_t d, uint32_t E, const float* dl, const f
   auto go = [&](auto kern) {
     if (smem > 48 * 1024)
       MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, GT, smem, st>>>(T, (int)d, (int)E, dl, x, dwg);
+    launch_pdl(kern, grid, GT, smem, st, T, (int)d, (int)E, dl, x, dwg);
   };
   const uint32_t ne = (E + 3) / 4;  // experts per thread
   if (ne <= 1) go(gate_wgrad_f32_kernel<1>);
@@ -193,7 +199,7 @@ void gate_dx_f32(uint64_t T, uint32_t d, uint32_t E, uint32_t k, const float* dl
     MOE_CUDA(cudaFuncSetAttribute(gate_dx_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
   dim3 grid((unsigned)ceil_div(T, DX_TOK), (unsigned)ceil_div(d, 64));
-  gate_dx_f32_kernel<<<grid, GT, smem, st>>>(T, (int)d, (int)E, (int)k, dl, wg, dXe, slot, dx);
+  launch_pdl(gate_dx_f32_kernel, grid, GT, smem, st, T, (int)d, (int)E, (int)k, dl, wg, dXe, slot, dx);
   MOE_LAUNCH_CHECK("gate_dx_f32_kernel");
   count_launch();
 }

@@ -49,6 +49,8 @@ struct Slice {
 // the narrow GEMMs whose 128 x 128 tiles leave SMs idle in the last wave).
 template <int KIND, int BMN, int EPI, int BNT>
 __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Args a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int BN = BNT, NH = BNT / 64;  // column halves of 64 per thread tile
   constexpr int C4 = BN / 4;              // float4 per B row of the slice ([k][n])
   __shared__ __align__(16) float As[2][BK][BM + PAD];
@@ -410,8 +412,8 @@ void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
   // wave (fewer than ~4 tiles per SM): c1's weight-gradient GEMMs
   const bool narrow = simt_use_bn64(p);
   auto go2 = [&](auto k128, auto k64) {
-    if (narrow) k64<<<grid, THREADS, 0, st>>>(a);
-    else k128<<<grid, THREADS, 0, st>>>(a);
+    if (narrow) launch_pdl(k64, grid, THREADS, 0, st, a);
+    else launch_pdl(k128, grid, THREADS, 0, st, a);
   };
   if (p.kind == MOE_GEMM_RAGGED_K) {
     if (p.epilogue == MOE_EPI_ATOMIC_ADD) go2(simt_gemm_kernel<1, 0, MOE_EPI_ATOMIC_ADD, 128>, simt_gemm_kernel<1, 0, MOE_EPI_ATOMIC_ADD, 64>);

@@ -242,6 +242,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     else tmem_alloc(tmem_hold, C_::TMEM_COLS);
     tc_fence_before();
   }
+  // everything above touched only this CTA's shared memory / TMEM: wait for
+  // the previous kernel here (PDL), then let the next one start launching
+  pdl_wait();
+  pdl_trigger();
   int* scratch = reinterpret_cast<int*>(smem);  // stage 0 is free during setup
   if (KIND == 0) {
     for (int g = threadIdx.x; g < G; g += THREADS) {
@@ -900,20 +904,22 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   const int budget = gemm_cta_budget();
   const int grid = budget > 0 ? std::min(budget, num_sms()) : num_sms();
   if (CG == 1) {
-    kern<<<grid, THREADS, C_::SMEM, st>>>(ta, tb, tcm, tc2, tax, a, ro);
+    launch_pdl(kern, grid, THREADS, C_::SMEM, st, ta, tb, tcm, tc2, tax, a, ro);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)std::max(2, grid & ~1));
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = C_::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     MOE_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tc2, tax, a, ro));
   }
   MOE_LAUNCH_CHECK("tc_gemm_kernel");

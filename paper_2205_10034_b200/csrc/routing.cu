@@ -90,6 +90,8 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
     uint64_t T, int E, int k, const float* __restrict__ logits, int32_t* __restrict__ expert,
     float* __restrict__ gate, int32_t* __restrict__ rank_local, int32_t* __restrict__ chunk_cnt,
     float* __restrict__ psum_part, uint64_t nchunks) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float tile[];  // [CHUNK][TS]
   __shared__ int hist[2][8][MAX_E];
   __shared__ float pw[8][MAX_E];
@@ -243,6 +245,8 @@ __global__ void __launch_bounds__(256) route_scan_kernel(
     int32_t* __restrict__ chunk_off, const float* __restrict__ psum_part, uint64_t nchunks,
     int32_t* __restrict__ count1, int32_t* __restrict__ count2, int32_t* __restrict__ kept,
     float* __restrict__ psum_e) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (e >= E) return;
@@ -275,6 +279,8 @@ __global__ void route_finalize_kernel(uint64_t T, int E, int k, uint64_t C, uint
                                       int32_t* __restrict__ position, uint8_t* __restrict__ keep,
                                       const float* __restrict__ psum_e,
                                       const int32_t* __restrict__ count1, float* __restrict__ aux) {
+  pdl_wait();
+  pdl_trigger();
   if (blockIdx.x == 0 && threadIdx.x < 32) {
     const double invT = T ? 1.0 / (double)T : 0.0;
     double a = 0.0;
@@ -315,16 +321,16 @@ void route_forward(uint64_t T, uint32_t E, uint32_t k, uint64_t C, const float* 
                                 SLAB_SMEM));
   const uint64_t nch = route_chunks(T);
   float* psum_e = ws.psum_part + nch * E;
-  route_topk_kernel<<<(unsigned)nch, RT_THREADS, SLAB_SMEM, st>>>(
+  launch_pdl(route_topk_kernel, (unsigned)nch, RT_THREADS, SLAB_SMEM, st, 
       T, (int)E, (int)k, logits, out.expert, out.gate, ws.rank_local, ws.chunk_cnt, ws.psum_part,
       nch);
   MOE_LAUNCH_CHECK("route_topk_kernel");
-  route_scan_kernel<<<(E + 7) / 8, 256, 0, st>>>(T, (int)E, (int)k, C, ws.chunk_cnt, ws.chunk_off,
+  launch_pdl(route_scan_kernel, (E + 7) / 8, 256, 0, st, T, (int)E, (int)k, C, ws.chunk_cnt, ws.chunk_off,
                                                  ws.psum_part, nch, out.count1, out.count2,
                                                  out.kept, psum_e);
   MOE_LAUNCH_CHECK("route_scan_kernel");
   const uint64_t n = T * k;
-  route_finalize_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+  launch_pdl(route_finalize_kernel, (unsigned)((n + 255) / 256), 256, 0, st, 
       T, (int)E, (int)k, C, nch, out.expert, ws.rank_local, ws.chunk_off, out.position, out.keep,
       psum_e, out.count1, out.aux_loss);
   MOE_LAUNCH_CHECK("route_finalize_kernel");
@@ -370,6 +376,8 @@ __global__ void dispatch_kernel(uint64_t T_, int d, int E, int k, uint64_t Cs, u
                                 const int32_t* __restrict__ position, T* __restrict__ buf,
                                 int32_t* __restrict__ slot, uint32_t pad,
                                 const int32_t* __restrict__ kept) {
+  pdl_wait();
+  pdl_trigger();
   zero_pad_rows(d, E, Cs, pad, kept, buf);
   const int lane = threadIdx.x & 31;
   const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -408,6 +416,8 @@ __global__ void dispatch_kernel(uint64_t T_, int d, int E, int k, uint64_t Cs, u
 template <typename T>
 __global__ void zero_pad_kernel(int d, uint64_t Cs, uint32_t pad, const int32_t* __restrict__ kept,
                                 T* __restrict__ buf) {
+  pdl_wait();
+  pdl_trigger();
   const int e = blockIdx.x;
   const int n = kept[e];
   const int end = (int)min((uint64_t)((n + pad - 1) / pad) * pad, Cs);
@@ -457,6 +467,8 @@ template <typename T>
 __global__ void combine_kernel(uint64_t T_, int d, int k, const T* __restrict__ Y,
                                const int32_t* __restrict__ slot, const float* __restrict__ gate,
                                T* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= T_) return;
@@ -486,6 +498,8 @@ __global__ void combine_bwd_kernel(uint64_t T_, int d, int k, const T* __restric
                                    const float* __restrict__ gate, T* __restrict__ dY,
                                    float* __restrict__ dgate, int E, uint64_t Cs, uint32_t pad,
                                    const int32_t* __restrict__ kept) {
+  pdl_wait();
+  pdl_trigger();
   zero_pad_rows(d, E, Cs, pad, kept, dY);
   const int lane = threadIdx.x & 31;
   const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -518,6 +532,8 @@ template <typename T>
 __global__ void gather_dx_kernel(uint64_t T_, int d, int k, const T* __restrict__ dXe,
                                  const int32_t* __restrict__ slot, const float* __restrict__ dxg,
                                  T* __restrict__ dx) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const uint64_t t = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (t >= T_) return;
@@ -554,6 +570,8 @@ __global__ void __launch_bounds__(RT_THREADS) route_bwd_kernel(
     const uint8_t* __restrict__ keep, const int32_t* __restrict__ count1,
     const float* __restrict__ dgate, float d_aux, float* __restrict__ dl_f32,
     LP* __restrict__ dl_lp, int ld, float* __restrict__ dbg) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float tile[];  // [CHUNK][TS]
   __shared__ float a_s[MAX_E];
   __shared__ float cs[8][SLAB];
@@ -656,6 +674,8 @@ template <typename T>
 __global__ void colsum_kernel(const int32_t* __restrict__ gm, const int32_t* __restrict__ ga,
                               const int32_t* __restrict__ gb, int N, const T* __restrict__ X,
                               float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int g = blockIdx.x;
   const int rows = gm[g];
   const int r0 = blockIdx.y * 128;
@@ -673,6 +693,8 @@ __global__ void colsum_kernel(const int32_t* __restrict__ gm, const int32_t* __r
 __global__ void colsum_bf16x8_kernel(const int32_t* __restrict__ gm, const int32_t* __restrict__ ga,
                                      const int32_t* __restrict__ gb, int N,
                                      const __nv_bfloat16* __restrict__ X, float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int g = blockIdx.x;
   const int rows = gm[g];
   const int r0 = blockIdx.y * 64;
@@ -721,6 +743,8 @@ __global__ void __launch_bounds__(CS_LANES * 32) colsum_group_bf16_kernel(
     const int32_t* __restrict__ gm, const int32_t* __restrict__ ga, const int32_t* __restrict__ gb,
     int N, int maxch, const __nv_bfloat16* __restrict__ X, float* __restrict__ out,
     float* __restrict__ part_ws, int32_t* __restrict__ ticket) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float part[CS_LANES][256 + 8];
   __shared__ int last;
   const int g = blockIdx.x / maxch, ch = blockIdx.x % maxch;
@@ -799,6 +823,8 @@ __global__ void __launch_bounds__(CS_LANES * 32) colsum_group_bf16_kernel(
 __global__ void build_groups_kernel(uint32_t P, uint32_t El, uint64_t Cs, const int32_t* cnt,
                                    int32_t* gm, int32_t* ga, int32_t* gb, int32_t* gm_k,
                                    int32_t* ga_k, int32_t* gb_k) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= P * El) return;
   const uint32_t s = g / El, j = g % El;
@@ -821,19 +847,19 @@ void dispatch_tokens(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C,
   const unsigned blocks = (unsigned)std::min<uint64_t>(ceil_div(T, 8), (uint64_t)num_sms() * 8);
   if (T) {
     if (dt == MOE_DTYPE_BF16)
-      dispatch_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+      launch_pdl(dispatch_kernel<__nv_bfloat16>, blocks, 256, 0, st, 
           T, d, E, k, Cs, C, (const __nv_bfloat16*)x, expert, position, (__nv_bfloat16*)buf, slot,
           pad, kept);
     else
-      dispatch_kernel<float><<<blocks, 256, 0, st>>>(T, d, E, k, Cs, C, (const float*)x, expert,
+      launch_pdl(dispatch_kernel<float>, blocks, 256, 0, st, T, d, E, k, Cs, C, (const float*)x, expert,
                                                      position, (float*)buf, slot, pad, kept);
     MOE_LAUNCH_CHECK("dispatch_kernel");
     count_launch();
   } else if (pad > 1) {
     if (dt == MOE_DTYPE_BF16)
-      zero_pad_kernel<__nv_bfloat16><<<E, 256, 0, st>>>(d, Cs, pad, kept, (__nv_bfloat16*)buf);
+      launch_pdl(zero_pad_kernel<__nv_bfloat16>, E, 256, 0, st, d, Cs, pad, kept, (__nv_bfloat16*)buf);
     else
-      zero_pad_kernel<float><<<E, 256, 0, st>>>(d, Cs, pad, kept, (float*)buf);
+      launch_pdl(zero_pad_kernel<float>, E, 256, 0, st, d, Cs, pad, kept, (float*)buf);
     MOE_LAUNCH_CHECK("zero_pad_kernel");
     count_launch();
   }
@@ -844,10 +870,10 @@ void combine_tokens(uint64_t T, uint32_t d, uint32_t k, moe_dtype_t dt, const vo
   if (!T) return;
   const unsigned blocks = (unsigned)ceil_div(T, 8);
   if (dt == MOE_DTYPE_BF16)
-    combine_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(T, d, k, (const __nv_bfloat16*)Y, slot,
+    launch_pdl(combine_kernel<__nv_bfloat16>, blocks, 256, 0, st, T, d, k, (const __nv_bfloat16*)Y, slot,
                                                           gate, (__nv_bfloat16*)y);
   else
-    combine_kernel<float><<<blocks, 256, 0, st>>>(T, d, k, (const float*)Y, slot, gate, (float*)y);
+    launch_pdl(combine_kernel<float>, blocks, 256, 0, st, T, d, k, (const float*)Y, slot, gate, (float*)y);
   MOE_LAUNCH_CHECK("combine_kernel");
   count_launch();
 }
@@ -860,20 +886,20 @@ void combine_backward(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C
   if (T) {
     const unsigned blocks = (unsigned)ceil_div(T, 8);
     if (dt == MOE_DTYPE_BF16)
-      combine_bwd_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+      launch_pdl(combine_bwd_kernel<__nv_bfloat16>, blocks, 256, 0, st, 
           T, d, k, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)Y, slot, gate,
           (__nv_bfloat16*)dY, dgate, (int)E, Cs, pad, kept);
     else
-      combine_bwd_kernel<float><<<blocks, 256, 0, st>>>(T, d, k, (const float*)dy,
+      launch_pdl(combine_bwd_kernel<float>, blocks, 256, 0, st, T, d, k, (const float*)dy,
                                                         (const float*)Y, slot, gate, (float*)dY,
                                                         dgate, (int)E, Cs, pad, kept);
     MOE_LAUNCH_CHECK("combine_bwd_kernel");
     count_launch();
   } else if (pad > 1) {
     if (dt == MOE_DTYPE_BF16)
-      zero_pad_kernel<__nv_bfloat16><<<E, 256, 0, st>>>(d, Cs, pad, kept, (__nv_bfloat16*)dY);
+      launch_pdl(zero_pad_kernel<__nv_bfloat16>, E, 256, 0, st, d, Cs, pad, kept, (__nv_bfloat16*)dY);
     else
-      zero_pad_kernel<float><<<E, 256, 0, st>>>(d, Cs, pad, kept, (float*)dY);
+      launch_pdl(zero_pad_kernel<float>, E, 256, 0, st, d, Cs, pad, kept, (float*)dY);
     MOE_LAUNCH_CHECK("zero_pad_kernel");
     count_launch();
   }
@@ -884,10 +910,10 @@ void gather_dx(uint64_t T, uint32_t d, uint32_t k, moe_dtype_t dt, const void* d
   if (!T) return;
   const unsigned blocks = (unsigned)ceil_div(T, 8);
   if (dt == MOE_DTYPE_BF16)
-    gather_dx_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+    launch_pdl(gather_dx_kernel<__nv_bfloat16>, blocks, 256, 0, st, 
         T, d, k, (const __nv_bfloat16*)dXe, slot, dx_gate, (__nv_bfloat16*)dx);
   else
-    gather_dx_kernel<float><<<blocks, 256, 0, st>>>(T, d, k, (const float*)dXe, slot, dx_gate,
+    launch_pdl(gather_dx_kernel<float>, blocks, 256, 0, st, T, d, k, (const float*)dXe, slot, dx_gate,
                                                     (float*)dx);
   MOE_LAUNCH_CHECK("gather_dx_kernel");
   count_launch();
@@ -904,11 +930,11 @@ void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, con
   MOE_CUDA(cudaFuncSetAttribute(route_bwd_kernel<float>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SLAB_SMEM));
   if (dlogits_lp && lp_dtype == MOE_DTYPE_BF16)
-    route_bwd_kernel<__nv_bfloat16><<<blocks, RT_THREADS, SLAB_SMEM, st>>>(
+    launch_pdl(route_bwd_kernel<__nv_bfloat16>, blocks, RT_THREADS, SLAB_SMEM, st, 
         T, (int)E, (int)k, logits, expert, gate, keep, count1, dgate, d_aux, dlogits_f32,
         (__nv_bfloat16*)dlogits_lp, (int)ld, dbg);
   else
-    route_bwd_kernel<float><<<blocks, RT_THREADS, SLAB_SMEM, st>>>(T, (int)E, (int)k, logits, expert, gate, keep,
+    launch_pdl(route_bwd_kernel<float>, blocks, RT_THREADS, SLAB_SMEM, st, T, (int)E, (int)k, logits, expert, gate, keep,
                                                     count1, dgate, d_aux, dlogits_f32,
                                                     (float*)dlogits_lp, (int)ld, dbg);
   MOE_LAUNCH_CHECK("route_bwd_kernel");
@@ -928,8 +954,8 @@ void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const i
   if (dt == MOE_DTYPE_BF16 && N % 8 == 0 && groups == num_b && part_ws && ticket) {
     // one group per expert (N = 1 and the P2P exchange): gb is a permutation
     const int maxch = (int)std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)CS_CHUNK));
-    colsum_group_bf16_kernel<<<dim3(groups * maxch, (unsigned)ceil_div(N, 256)), CS_LANES * 32, 0,
-                               st>>>(gm, ga, gb, (int)N, maxch, (const __nv_bfloat16*)X, out,
+    launch_pdl(colsum_group_bf16_kernel, dim3(groups * maxch, (unsigned)ceil_div(N, 256)), CS_LANES * 32, 0,
+                               st, gm, ga, gb, (int)N, maxch, (const __nv_bfloat16*)X, out,
                                      part_ws, ticket);
     MOE_LAUNCH_CHECK("colsum_group_bf16_kernel");
     count_launch();
@@ -938,14 +964,14 @@ void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const i
   MOE_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (uint64_t)num_b * N, st));
   if (dt == MOE_DTYPE_BF16 && N % 8 == 0) {
     dim3 grid(groups, (unsigned)ceil_div(max_rows, 64), (unsigned)ceil_div(N / 8, 128));
-    colsum_bf16x8_kernel<<<grid, 128, 0, st>>>(gm, ga, gb, (int)N, (const __nv_bfloat16*)X, out);
+    launch_pdl(colsum_bf16x8_kernel, grid, 128, 0, st, gm, ga, gb, (int)N, (const __nv_bfloat16*)X, out);
   } else {
     dim3 grid(groups, (unsigned)ceil_div(max_rows, 128), (unsigned)ceil_div(N, 256));
     if (dt == MOE_DTYPE_BF16)
-      colsum_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(gm, ga, gb, (int)N,
+      launch_pdl(colsum_kernel<__nv_bfloat16>, grid, 256, 0, st, gm, ga, gb, (int)N,
                                                          (const __nv_bfloat16*)X, out);
     else
-      colsum_kernel<float><<<grid, 256, 0, st>>>(gm, ga, gb, (int)N, (const float*)X, out);
+      launch_pdl(colsum_kernel<float>, grid, 256, 0, st, gm, ga, gb, (int)N, (const float*)X, out);
   }
   MOE_LAUNCH_CHECK("colsum_kernel");
   count_launch();
@@ -955,7 +981,7 @@ void build_groups(uint32_t P, uint32_t El, uint64_t Cs, const int32_t* cnt, int3
                   int32_t* ga, int32_t* gb, int32_t* gm_k, int32_t* ga_k, int32_t* gb_k,
                   cudaStream_t st) {
   const uint32_t n = P * El;
-  build_groups_kernel<<<(n + 255) / 256, 256, 0, st>>>(P, El, Cs, cnt, gm, ga, gb, gm_k, ga_k,
+  launch_pdl(build_groups_kernel, (n + 255) / 256, 256, 0, st, P, El, Cs, cnt, gm, ga, gb, gm_k, ga_k,
                                                        gb_k);
   MOE_LAUNCH_CHECK("build_groups_kernel");
   count_launch();
