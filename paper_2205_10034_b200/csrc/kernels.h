@@ -99,7 +99,7 @@ void gather_dx(uint64_t T, uint32_t d, uint32_t k, moe_dtype_t dt, const void* d
 
 // Column sums over the valid rows of each (source, expert) slot group:
 // out[b][n] = sum over groups g with gb[g]==b of sum_{r<m[g]} X[a_row[g]+r][n].
-// With one group per b (bf16), deterministic: row chunks of 512 rows reduce
+// With one group per b (bf16), deterministic: row chunks of 256 rows reduce
 // through part_ws (colsum_ws_floats) in chunk order; ticket
 // (colsum_ticket_ints, zeroed once) re-arms itself.
 uint64_t colsum_ws_floats(uint32_t groups, uint32_t N, uint64_t max_rows);

@@ -737,7 +737,10 @@ constexpr int CS_LANES = 16;
 // block) to finish -- an acq_rel ticket -- sums them in chunk order, so db2 is
 // deterministic and a heavily loaded expert (skewed routing) is spread over
 // many blocks instead of serialising on one.
-constexpr int CS_CHUNK = 512;
+#ifndef MOE_CS_CHUNK
+#define MOE_CS_CHUNK 256  // A/B: c3 db2 22 -> 20 us vs 512, 1024 slower (30 us)
+#endif
+constexpr int CS_CHUNK = MOE_CS_CHUNK;
 
 __global__ void __launch_bounds__(CS_LANES * 32) colsum_group_bf16_kernel(
     const int32_t* __restrict__ gm, const int32_t* __restrict__ ga, const int32_t* __restrict__ gb,
