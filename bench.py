@@ -238,6 +238,10 @@ def main():
     ap.add_argument("--tokens", type=int, default=0, help="override T (tokens per GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--placement", default="round_robin", choices=["contiguous", "round_robin"],
+                    help="expert placement over the N GPUs (include/moe_b200.h); round-robin "
+                         "spreads a skewed gate's hot experts over the ranks (c3 N=4: 2.3x), "
+                         "neutral for uniform routing (c2)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="EP token exchange for N>1: NVLink peer stores (p2p) or NCCL all-to-all")
     args = ap.parse_args()
@@ -266,7 +270,7 @@ def main():
     dtype = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
     E, k, d, dff, T, cf = cfg["E"], cfg["k"], cfg["d"], cfg["dff"], cfg["T"], cfg["cf"]
     mcfg = MoEConfig(E, k, d, dff, cf, T, dtype, gate_bias=bool(cfg.get("skew")),
-                     exchange=args.exchange)
+                     exchange=args.exchange, placement=args.placement)
     layer = MoELayer(mcfg, ep=ep, device=dev)
     gb = None
     if cfg.get("skew"):
@@ -469,6 +473,7 @@ def main():
                    "capacity": layer.capacity, "experts_per_gpu": E // ws,
                    "parallelism": f"ep{ws}" if ws > 1 else "single",
                    "exchange": args.exchange if ws > 1 else None,
+                   "placement": args.placement if ws > 1 else None,
                    "l2": "inputs larger than L2 (x 128 MiB + weights 1 GiB per step), no flush"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks,

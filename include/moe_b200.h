@@ -240,7 +240,17 @@ typedef struct moe_layer_desc {
   uint32_t ep_rank;
   void* nccl_comm;         /* ncclComm_t when ep_size > 1 (see moe_comm_*) */
   uint32_t exchange;       /* ep_size > 1: MOE_EXCHANGE_P2P (default) or MOE_EXCHANGE_NCCL */
+  uint32_t placement;      /* ep_size > 1: MOE_PLACEMENT_CONTIGUOUS (default) or _ROUND_ROBIN */
 } moe_layer_desc_t;
+
+/* Expert placement over the ep_size ranks.  CONTIGUOUS: expert e lives on rank
+ * e / (E/P) as local expert e % (E/P).  ROUND_ROBIN: on rank e % P as local
+ * expert e / P, so a skewed (Zipf-like) routing distribution whose hot experts
+ * have neighbouring ids is spread over all ranks instead of landing on rank 0.
+ * Routing semantics (positions, capacity, outputs) do not depend on it; the
+ * caller passes the weights of this rank's local experts in local order. */
+#define MOE_PLACEMENT_CONTIGUOUS 0
+#define MOE_PLACEMENT_ROUND_ROBIN 1
 
 /* EP token exchange.  P2P: the dispatch / combine-backward kernels store rows
  * straight into the peers' receive buffers over NVLink (CUDA IPC mappings,

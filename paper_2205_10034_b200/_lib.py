@@ -160,6 +160,7 @@ class LayerDesc(C.Structure):
         ("ep_rank", C.c_uint32),
         ("nccl_comm", C.c_void_p),
         ("exchange", C.c_uint32),
+        ("placement", C.c_uint32),
     ]
 
 

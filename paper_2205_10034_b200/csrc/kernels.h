@@ -109,6 +109,11 @@ void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const i
                   cudaStream_t st, uint64_t max_rows, float* part_ws = nullptr,
                   int32_t* ticket = nullptr);
 
+// Round-robin placement relabel (include/moe_b200.h): pexpert = pi(expert),
+// pkept[pi(e)] = kept[e], pi(e) = (e % P) * (E / P) + e / P.
+void relabel_experts(uint64_t T, uint32_t k, uint32_t E, uint32_t P, const int32_t* expert,
+                     const int32_t* kept, int32_t* pexpert, int32_t* pkept, cudaStream_t st);
+
 // Build the expert GEMM group tables for P source ranks x El local experts from
 // the received kept counts cnt[s][j]: group g = s*El + j, m = cnt, a_row =
 // (s*El+j)*Cs (Cs = slot stride), b = j.  Also the RAGGED_K order (grouped by

@@ -69,6 +69,8 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   config_check(E % P == 0, "layer.ep_size: must divide num_experts");
   config_check(rank < P, "layer.ep_rank: must be < ep_size");
   config_check(P == 1 || d.nccl_comm != nullptr, "layer.nccl_comm: required when ep_size > 1");
+  config_check(d.placement == MOE_PLACEMENT_CONTIGUOUS || d.placement == MOE_PLACEMENT_ROUND_ROBIN,
+               "layer.placement: must be MOE_PLACEMENT_CONTIGUOUS or MOE_PLACEMENT_ROUND_ROBIN");
   if (dt == MOE_DTYPE_BF16) {
     config_check(dm % 128 == 0, "layer.d_model: bf16 path needs a multiple of 128");
     config_check(dff % 128 == 0, "layer.d_ff: bf16 path needs a multiple of 128");
@@ -99,6 +101,11 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   count2 = dalloc<int32_t>(owned, E);
   kept = dalloc<int32_t>(owned, E);
   aux = dalloc<float>(owned, 1);
+  rr = d.placement == MOE_PLACEMENT_ROUND_ROBIN && P > 1;
+  if (rr) {
+    pexpert = dalloc<int32_t>(owned, T * k);
+    pkept = dalloc<int32_t>(owned, E);
+  }
   rws.nchunks = route_chunks(T);
   rws.chunk_cnt = dalloc<int32_t>(owned, 2 * rws.nchunks * E);
   rws.chunk_off = dalloc<int32_t>(owned, 2 * rws.nchunks * E);
@@ -285,24 +292,25 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   // K2: routing
   moe_routing_out_t ro{expert, gate, position, keep, count1, count2, kept, aux};
   route_forward(T, E, k, C, logits, ro, rws, st);
+  if (rr) relabel_experts(T, k, E, P, expert, kept, pexpert, pkept, st);
   mark("route", st);
   // K3 (+K4 in P2P mode): dispatch into the Fusion-packed send buffer, or
   // straight into the owning ranks' receive buffers over NVLink
   if (p2p) {
-    p2p_counts(win, kept, ph, st);
+    p2p_counts(win, dkept(), ph, st);
     p2p_wait(win, SLOT_CNT, ph, st);
-    p2p_dispatch(win, T, dm, k, C, dt, x, expert, position, slot, ph, st);
+    p2p_dispatch(win, T, dm, k, C, dt, x, dexp(), position, slot, ph, st);
     mark("dispatch_p2p", st);
     p2p_wait(win, SLOT_DISPATCH, ph, st);
     p2p_local_groups(win, gm, ga, gb, xr, st);
   } else {
-    dispatch_tokens(T, dm, E, k, C, pad, dt, x, expert, position, kept, xs, slot, st);
+    dispatch_tokens(T, dm, E, k, C, pad, dt, x, dexp(), position, dkept(), xs, slot, st);
     mark("dispatch", st);
   }
   // K4: counts + payload exchange (one message per peer)
   if (P > 1 && !p2p) {
     MOE_NCCL(ncclGroupStart());
-    a2a(kept, cnt_recv, El * sizeof(int32_t), st);
+    a2a(dkept(), cnt_recv, El * sizeof(int32_t), st);
     a2a(xs, xr, El * Cs * dm * esz, st);
     MOE_NCCL(ncclGroupEnd());
   }
@@ -386,9 +394,9 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   // or straight into the owning ranks' receive buffers (P2P)
   if (p2p) {
     p2p_wait(win, SLOT_PHASE, ph - 1, st);
-    p2p_combine_bwd(win, T, dm, k, dt, dy, slot, gate, expert, position, dgate, ph, st);
+    p2p_combine_bwd(win, T, dm, k, dt, dy, slot, gate, dexp(), position, dgate, ph, st);
   } else {
-    combine_backward(T, dm, E, k, C, pad, dt, dy, Yh, slot, gate, kept, dYs, dgate, st);
+    combine_backward(T, dm, E, k, C, pad, dt, dy, Yh, slot, gate, dkept(), dYs, dgate, st);
   }
   mark("combine_bwd", st);
   // K2^T: dlogits

@@ -61,6 +61,11 @@ struct Layer {
   int32_t* cnt_recv = nullptr;
   int32_t *gm = nullptr, *ga = nullptr, *gb = nullptr, *gmk = nullptr, *gak = nullptr,
           *gbk = nullptr;
+  // round-robin placement: physical expert ids / kept counts for the exchange
+  bool rr = false;
+  int32_t *pexpert = nullptr, *pkept = nullptr;
+  const int32_t* dexp() const { return rr ? pexpert : expert; }
+  const int32_t* dkept() const { return rr ? pkept : kept; }
   float* cs_part = nullptr;      // db2 chunk partials (group_colsum)
   int32_t* cs_ticket = nullptr;  // db2 chunk tickets, self re-arming
   void *Gp = nullptr, *Aact = nullptr, *Yl = nullptr, *Yh = nullptr;

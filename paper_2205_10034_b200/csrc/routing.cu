@@ -980,6 +980,34 @@ void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const i
   count_launch();
 }
 
+// Round-robin expert placement: physical expert id pi(e) = (e % P) * El + e / P
+// (rank e % P, local expert e / P), so the contiguous-placement exchange and
+// slot layout downstream serve it unchanged.  pexpert = pi(expert) (-1 kept),
+// pkept[pi(e)] = kept[e].
+__global__ void relabel_experts_kernel(uint64_t n, uint32_t E, uint32_t P,
+                                       const int32_t* __restrict__ expert,
+                                       const int32_t* __restrict__ kept,
+                                       int32_t* __restrict__ pexpert, int32_t* __restrict__ pkept) {
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t El = E / P;
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < E) pkept[(i % P) * El + i / P] = kept[i];
+  if (i < n) {
+    const int32_t e = expert[i];
+    pexpert[i] = e < 0 ? e : (int32_t)((e % P) * El + e / P);
+  }
+}
+
+void relabel_experts(uint64_t T, uint32_t k, uint32_t E, uint32_t P, const int32_t* expert,
+                     const int32_t* kept, int32_t* pexpert, int32_t* pkept, cudaStream_t st) {
+  const uint64_t n = std::max<uint64_t>(T * k, E);
+  launch_pdl(relabel_experts_kernel, (unsigned)ceil_div(n, 256), 256, 0, st, T * k, E, P, expert,
+             kept, pexpert, pkept);
+  MOE_LAUNCH_CHECK("relabel_experts_kernel");
+  count_launch();
+}
+
 void build_groups(uint32_t P, uint32_t El, uint64_t Cs, const int32_t* cnt, int32_t* gm,
                   int32_t* ga, int32_t* gb, int32_t* gm_k, int32_t* ga_k, int32_t* gb_k,
                   cudaStream_t st) {

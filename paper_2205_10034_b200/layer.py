@@ -70,6 +70,7 @@ class MoEConfig:
     dtype: torch.dtype = torch.bfloat16
     gate_bias: bool = False
     exchange: str = "p2p"  # EP token exchange: "p2p" (NVLink peer stores) or "nccl"
+    placement: str = "contiguous"  # expert placement over ranks: "contiguous" or "round_robin"
 
 
 class EPGroup:
@@ -129,6 +130,9 @@ class MoELayer:
         if cfg.exchange not in ("p2p", "nccl"):
             raise _lib.ConfigError("layer.exchange: must be 'p2p' or 'nccl'")
         desc.exchange = 0 if cfg.exchange == "p2p" else 1
+        if cfg.placement not in ("contiguous", "round_robin"):
+            raise _lib.ConfigError("layer.placement: must be 'contiguous' or 'round_robin'")
+        desc.placement = 0 if cfg.placement == "contiguous" else 1
         h = C.c_void_p()
         if self.device.type == "cuda":
             with torch.cuda.device(self.device):
@@ -138,6 +142,11 @@ class MoELayer:
         self._h = h
         self.capacity = int(lib.moe_layer_capacity(h))
         self.El = cfg.num_experts // self.P
+        # global expert id of each local expert (include/moe_b200.h placement)
+        if cfg.placement == "round_robin":
+            self.local_experts = [j * self.P + self.rank for j in range(self.El)]
+        else:
+            self.local_experts = [self.rank * self.El + j for j in range(self.El)]
         self.params: Dict[str, torch.Tensor] = {}
         self.grads: Dict[str, torch.Tensor] = {}
 
@@ -159,7 +168,7 @@ class MoELayer:
         if gate_bias is not None:
             p["bg"].copy_(gate_bias)
         for j in range(El):
-            e = self.rank * El + j  # global expert id: identical weights for any ep_size
+            e = self.local_experts[j]  # global expert id: identical weights for any ep_size
             fill_uniform(p["w1"][j], substream_seed(seed, T_W1, e), -bd, bd)
             fill_uniform(p["b1"][j], substream_seed(seed, T_B1, e), -bd, bd)
             fill_uniform(p["w2"][j], substream_seed(seed, T_W2, e), -bf, bf)

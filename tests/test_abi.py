@@ -90,3 +90,12 @@ def test_layer_config_errors_name_the_field():
                       tokens=16, dtype=1, has_gate_bias=0, ep_size=4, ep_rank=0, nccl_comm=None)
         h = C.c_void_p()
         call("moe_layer_create", C.byref(d), C.byref(h))
+    with pytest.raises(ConfigError, match="layer.placement"):
+        MoELayer(MoEConfig(8, 1, 128, 256, 1.25, 64, torch.bfloat16, placement="striped"),
+                 device="cpu")
+    with pytest.raises(ConfigError, match="layer.placement"):
+        d = LayerDesc(num_experts=8, top_k=1, d_model=128, d_ff=256, capacity_factor=1.0,
+                      tokens=16, dtype=1, has_gate_bias=0, ep_size=1, ep_rank=0, nccl_comm=None,
+                      exchange=0, placement=7)
+        h = C.c_void_p()
+        call("moe_layer_create", C.byref(d), C.byref(h))

@@ -98,8 +98,9 @@ def _worker(rank, world, port, case, q):
             gb.close()
             q.put((rank, "ok"))
             return
-        E, k, d, dff, T, dt, exch = case
-        cfg = MoEConfig(E, k, d, dff, 1.25, T, dt, exchange=exch)
+        E, k, d, dff, T, dt, exch = case[:7]
+        placement = case[7] if len(case) > 7 else "contiguous"
+        cfg = MoEConfig(E, k, d, dff, 1.25, T, dt, exchange=exch, placement=placement)
         lep = MoELayer(cfg, ep=ep)
         lep.init_params(99)
         x = lep.make_input(99)
@@ -123,7 +124,8 @@ def _worker(rank, world, port, case, q):
         g1 = {n: t.clone() for n, t in l1.grads.items()}
         for n in g1:
             dist.all_reduce(g1[n])  # sum over ranks of the single-GPU gradients
-        sl = slice(rank * El, (rank + 1) * El)
+        sl = lep.local_experts  # global ids of this rank's experts (placement)
+        assert len(sl) == El
         for n in ("dw1", "db1", "dw2", "db2"):
             ref = g1[n][sl]
             err = (lep.grads[n] - ref).abs().max() / ref.abs().max()
@@ -181,6 +183,18 @@ def test_gradient_buckets_allreduce():
 ])
 def test_ep_layer_matches_single_gpu(case):
     _run(case, world=min(torch.cuda.device_count(), 2))
+
+
+@pytest.mark.parametrize("case", [
+    (32, 2, 256, 512, 3000, torch.bfloat16, "p2p", "round_robin"),
+    (32, 2, 256, 512, 3000, torch.bfloat16, "nccl", "round_robin"),
+    (16, 1, 128, 256, 1000, torch.float32, "p2p", "round_robin"),
+])
+def test_ep_layer_round_robin_placement(case):
+    """Round-robin expert placement (expert e on rank e % P): EP output and dx
+    still bitwise equal to the single-GPU layer, weight gradients land on the
+    rank holding each expert."""
+    _run(case, world=min(torch.cuda.device_count(), 4))
 
 
 def _ep_sweep(n=4, seed=77):
