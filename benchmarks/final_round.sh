@@ -1,6 +1,6 @@
 # End-of-round sweep on one box (N GPUs): GPU tests, every config at N=1 and
 # N=2..NG, the reference arm, and the ncu evidence on GPU 0.
-TAG=${1:-r01z}
+TAG=${1:-r01z}; PROFILE=${2:-1}
 mkdir -p gpurun_out
 NG=$(nvidia-smi -L | wc -l)
 nvidia-smi --query-gpu=name,clocks.max.sm --format=csv,noheader | head -1
@@ -21,4 +21,4 @@ while [ $n -le $NG ]; do
   done
   n=$((n * 2))
 done
-CUDA_VISIBLE_DEVICES=0 bash benchmarks/profile_round.sh ${TAG} c2
+[ "$PROFILE" = 1 ] && CUDA_VISIBLE_DEVICES=0 bash benchmarks/profile_round.sh ${TAG} c2
