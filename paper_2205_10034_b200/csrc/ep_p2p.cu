@@ -450,21 +450,35 @@ void p2p_counts(const P2PWindow& w, const int32_t* kept, uint64_t epoch, cudaStr
   count_launch();
 }
 
-void p2p_allreduce_f32(const P2PWindow& w, float* a, uint64_t na, float* b, uint64_t nb,
-                       uint64_t epoch, cudaStream_t st) {
+static unsigned red_grid(uint64_t na, uint64_t nb) {
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(na / 4 + nb, 256),
+                                                            (uint64_t)num_sms()));
+}
+
+void p2p_allreduce_push(const P2PWindow& w, const float* a, uint64_t na, const float* b,
+                        uint64_t nb, uint64_t epoch, cudaStream_t st) {
   if (w.P <= 1) return;
   arg_check(na % 4 == 0 && na + nb <= w.n_red, "p2p_allreduce: gradient does not fit the window");
-  const unsigned grid = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>(ceil_div(na / 4 + nb, 256), (uint64_t)num_sms()));
-  p2p_red_push_kernel<<<grid, 256, 0, st>>>(win_of(w), w.off_red, w.n_red, ctr_of(w, 5), a, na,
-                                            b, nb, epoch);
+  p2p_red_push_kernel<<<red_grid(na, nb), 256, 0, st>>>(win_of(w), w.off_red, w.n_red,
+                                                        ctr_of(w, 5), a, na, b, nb, epoch);
   MOE_LAUNCH_CHECK("p2p_red_push_kernel");
   count_launch();
+}
+
+void p2p_allreduce_finish(const P2PWindow& w, float* a, uint64_t na, float* b, uint64_t nb,
+                          uint64_t epoch, cudaStream_t st) {
+  if (w.P <= 1) return;
   p2p_wait(w, SLOT_GRAD, epoch, st);
-  p2p_red_sum_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const float*>(w.base + w.off_red),
-                                           w.P, w.n_red, a, na, b, nb);
+  p2p_red_sum_kernel<<<red_grid(na, nb), 256, 0, st>>>(
+      reinterpret_cast<const float*>(w.base + w.off_red), w.P, w.n_red, a, na, b, nb);
   MOE_LAUNCH_CHECK("p2p_red_sum_kernel");
   count_launch();
+}
+
+void p2p_allreduce_f32(const P2PWindow& w, float* a, uint64_t na, float* b, uint64_t nb,
+                       uint64_t epoch, cudaStream_t st) {
+  p2p_allreduce_push(w, a, na, b, nb, epoch, st);
+  p2p_allreduce_finish(w, a, na, b, nb, epoch, st);
 }
 
 unsigned persistent_grid(uint64_t T) {

@@ -86,6 +86,12 @@ void p2p_push_home(const P2PWindow& w, uint64_t home_off, const void* src, int s
 // red[me] of every window (SLOT_GRAD := epoch), then sums red[0..P-1] in rank
 // order, so all replicas end bitwise identical.  Replaces ncclAllReduce for
 // the small gate gradients (latency, not bandwidth, bound).
+// The same in two halves: push this rank's partials (as soon as they are
+// final), finish = wait for every peer's push and sum in source order.
+void p2p_allreduce_push(const P2PWindow& w, const float* a, uint64_t na, const float* b,
+                        uint64_t nb, uint64_t epoch, cudaStream_t st);
+void p2p_allreduce_finish(const P2PWindow& w, float* a, uint64_t na, float* b, uint64_t nb,
+                          uint64_t epoch, cudaStream_t st);
 void p2p_allreduce_f32(const P2PWindow& w, float* a, uint64_t na, float* b, uint64_t nb,
                        uint64_t epoch, cudaStream_t st);
 

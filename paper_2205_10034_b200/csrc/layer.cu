@@ -436,6 +436,11 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.ldc = dm;
     grouped_gemm(p, st);
   }
+  // the replicated gate gradients are final here: push them to the peers now
+  // so the closing all-reduce only sums (no wait on a late peer's push)
+  if (p2p)
+    p2p_allreduce_push(win, g.dwg, (uint64_t)E * dm, desc.has_gate_bias ? g.dbg : nullptr,
+                       desc.has_gate_bias && g.dbg ? E : 0, ph, st);
   mark("gate_wgrad", st);
   if (p2p) {
     p2p_wait(win, SLOT_DY, ph, st);
@@ -563,9 +568,9 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   }
   mark("gate_dgrad_gather_dx", st);
   if (p2p) {
-    // replicated gate gradients: one-shot all-reduce over the peer windows
-    p2p_allreduce_f32(win, g.dwg, (uint64_t)E * dm, desc.has_gate_bias ? g.dbg : nullptr,
-                      desc.has_gate_bias && g.dbg ? E : 0, ph, st);
+    // replicated gate gradients: sum the pushed partials in rank order
+    p2p_allreduce_finish(win, g.dwg, (uint64_t)E * dm, desc.has_gate_bias ? g.dbg : nullptr,
+                         desc.has_gate_bias && g.dbg ? E : 0, ph, st);
   } else if (P > 1) {
     MOE_NCCL(ncclGroupStart());
     MOE_NCCL(ncclAllReduce(g.dwg, g.dwg, (uint64_t)E * dm, ncclFloat32, ncclSum, (ncclComm_t)comm, st));
