@@ -391,6 +391,36 @@ def main():
                         "hbm_GBps": gbs, "hbm_frac": gbs / pk["hbm_gbs"]})
     roof["per_gemm"] = per
 
+    # ---- HBM roofline of the memory-bound kernels (gating, dispatch, combine
+    # and their backward): algorithmic bytes = each operand read once + each
+    # output written once, R = kept rows of this rank's tokens,
+    # time = the phase's CUDA events (includes its launch gap).  At N > 1 the
+    # dispatch / combine-backward phases also carry the NVLink exchange and
+    # are reported under "nvlink" instead.
+    Rk = float(kept_local)
+    Ep = (E + 63) // 64 * 64 if dtype == torch.bfloat16 else E
+    hbytes = {
+        "gate_gemm": T * d * es + T * E * 4,                          # x -> logits (fp32)
+        "route": T * E * 4 + T * k * 13,                               # logits -> e, g, pos, keep
+        "dispatch": T * d * es + Rk * d * es,                          # x -> expert-major rows
+        "combine": Rk * d * es + T * d * es,                           # Y rows -> y
+        "combine_bwd": T * d * es + 2 * Rk * d * es,                   # dy, Y -> dY rows
+        "route_bwd": T * E * 4 + T * Ep * es,                          # logits -> dlogits
+        "bias_grads": Rk * d * es,                                     # dY -> db2
+        "gate_wgrad": T * d * es + T * Ep * es,                        # x, dlogits -> dWg
+        "gate_dgrad_gather_dx": T * Ep * es + Rk * d * es + T * d * es,  # dlogits, dXe -> dx
+    }
+    if ws > 1:  # the P2P combine backward pushes its rows over NVLink
+        hbytes.pop("combine_bwd")
+    hbm = []
+    for name, nbytes in hbytes.items():
+        ms_k = sum(v for n, v in phase_tot.items() if n.split(".", 1)[-1] == name) / args.steps
+        if ms_k > 0:
+            gbs = nbytes / (ms_k / 1000.0) / 1e9
+            hbm.append({"kernel": name, "us": 1000.0 * ms_k, "bytes": nbytes, "GBps": gbs,
+                        "frac": gbs / pk["hbm_gbs"]})
+    roof["hbm_kernels"] = hbm
+
     # ---- end to end through the host-buffer API (H2D + step + D2H) ----
     e2e = None
     if not args.no_e2e:
