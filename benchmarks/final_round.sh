@@ -21,4 +21,4 @@ while [ $n -le $NG ]; do
   done
   n=$((n * 2))
 done
-[ "$PROFILE" = 1 ] && CUDA_VISIBLE_DEVICES=0 bash benchmarks/profile_round.sh ${TAG} c2
+if [ "$PROFILE" = 1 ]; then CUDA_VISIBLE_DEVICES=0 bash benchmarks/profile_round.sh ${TAG} c2; fi
