@@ -81,6 +81,10 @@ __device__ __forceinline__ void load_slab(const float* __restrict__ logits, uint
   }
 }
 
+// exp(x) as one FMUL + MUFU.EX2 (max relative error ~2^-21, against
+// libdevice expf's ~10 instructions); exp(-inf) = 0, NaN stays NaN.
+__device__ __forceinline__ float exp_f(float x) { return ex2_approx(x * 1.44269504088896341f); }
+
 // Phase A: thread per token (the block is one 256-token chunk): top-k on the
 // fp32 logits, softmax, gates; per chunk: histograms (expert-major
 // [i][E][nchunks]), in-chunk ranks (warp match over 32 consecutive tokens +
@@ -114,15 +118,22 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
     load_slab(logits, t0, T, E, e0, ne, tile);
     __syncthreads();
     if (valid) {
+      // experts arrive in index order, so a tie can only displace the
+      // sentinel: (v > v1 || (v == v1 && e < i1)) == (v > v1 || i1 unset).
+      // Branchless selects instead of the divergent if / else-if chain.
       const float* row = tile + tid * TS;
+#pragma unroll 4
       for (int j = 0; j < ne; ++j) {
         const float v = row[j];
         const int e = e0 + j;
-        if (v > v1 || (v == v1 && e < i1)) {
-          v2 = v1; i2 = i1; v1 = v; i1 = e;
-        } else if (v > v2 || (v == v2 && e < i2)) {
-          v2 = v; i2 = e;
-        }
+        const bool c1 = v > v1 || i1 == 0x7fffffff;
+        const bool c2 = !c1 && (v > v2 || i2 == 0x7fffffff);
+        const float nv2 = c1 ? v1 : v;
+        const int ni2 = c1 ? i1 : e;
+        v2 = (c1 || c2) ? nv2 : v2;
+        i2 = (c1 || c2) ? ni2 : i2;
+        v1 = c1 ? v : v1;
+        i1 = c1 ? e : i1;
       }
     }
   }
@@ -135,9 +146,13 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
       load_slab(logits, t0, T, E, e0, ne, tile);
       __syncthreads();
     }
-    if (valid) {
-      const float* row = tile + tid * TS;
-      for (int j = 0; j < ne; ++j) z += expf(row[j] - v1);
+    if (valid) {  // one slab: keep exp(l - max) in the tile for pass 3
+      float* row = tile + tid * TS;
+      for (int j = 0; j < ne; ++j) {
+        const float ex = exp_f(row[j] - v1);
+        if (nslab == 1) row[j] = ex;
+        z += ex;
+      }
     }
   }
   const float inv = valid ? 1.0f / z : 0.f;
@@ -173,7 +188,10 @@ __global__ void __launch_bounds__(RT_THREADS) route_topk_kernel(
       if (t0 + r >= T) break;
       const float mj = mrow[r], ij = irow[r];
 #pragma unroll
-      for (int q = 0; q < SLAB / 32; ++q) acc[q] += expf(tile[r * TS + lane + 32 * q] - mj) * ij;
+      for (int q = 0; q < SLAB / 32; ++q) {
+        const float tv = tile[r * TS + lane + 32 * q];
+        acc[q] += (nslab == 1 ? tv : exp_f(tv - mj)) * ij;
+      }
     }
 #pragma unroll
     for (int q = 0; q < SLAB / 32; ++q)
@@ -598,9 +616,10 @@ __global__ void __launch_bounds__(RT_THREADS) route_bwd_kernel(
       load_slab(logits, t0, T_, E, e0, ne, tile);
       __syncthreads();
     }
-    if (valid)
+    if (valid)  // one slab: keep exp(l - max) in the tile for the next pass
       for (int j = 0; j < ne; ++j) {
-        const float ex = expf(tile[tid * TS + j] - m);
+        const float ex = exp_f(tile[tid * TS + j] - m);
+        if (nslab == 1) tile[tid * TS + j] = ex;
         z += ex;
         pnum = fmaf(ex, a_s[e0 + j], pnum);
       }
@@ -633,7 +652,8 @@ __global__ void __launch_bounds__(RT_THREADS) route_bwd_kernel(
       const int e = e0 + j;
       float v = 0.f;
       if (valid) {
-        const float pe = expf(tile[tid * TS + j] - m) * inv;
+        const float tv = tile[tid * TS + j];
+        const float pe = (nslab == 1 ? tv : exp_f(tv - m)) * inv;
         v = d_aux * pe * (a_s[e] - pa);
         if (k == 1) v += gterm * p1 * ((e == e1 ? 1.f : 0.f) - pe);
         else v += (e == e1 ? gterm : 0.f) - (e == e2 ? gterm : 0.f);
