@@ -758,7 +758,7 @@ constexpr int CS_LANES = 16;
 // deterministic and a heavily loaded expert (skewed routing) is spread over
 // many blocks instead of serialising on one.
 #ifndef MOE_CS_CHUNK
-#define MOE_CS_CHUNK 256  // A/B: c3 db2 22 -> 20 us vs 512, 1024 slower (30 us)
+#define MOE_CS_CHUNK 256  // A/B: c3 db2 22 -> 20 us vs 512, 1024 slower (30 us), 128 slower (c2 39 -> 43 us)
 #endif
 constexpr int CS_CHUNK = MOE_CS_CHUNK;
 
