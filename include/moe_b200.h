@@ -310,7 +310,9 @@ moe_status_t moe_layer_backward(moe_layer_t layer, const moe_layer_params_t* par
  * copy-in / compute / copy-out streams over double-buffered staging so that
  * consecutive calls overlap H2D, compute and D2H; `stream` is made to wait for
  * this step's D2H, i.e. outputs, gradients and the reuse of the host buffers
- * are safe once `stream` reaches this call.  Do not interleave with
+ * are safe once `stream` reaches this call; the step's compute waits for all
+ * work queued on `stream` before the call (e.g. an optimizer step that updates
+ * params from the previous step's grads).  Do not interleave with
  * moe_layer_forward/backward on the same layer without synchronising. */
 moe_status_t moe_layer_train_step_host(moe_layer_t layer, const moe_layer_params_t* params,
                                        const void* x_host, const void* dy_host, float d_aux,
@@ -323,6 +325,14 @@ moe_status_t moe_layer_train_step_host(moe_layer_t layer, const moe_layer_params
 moe_status_t moe_layer_set_profiling(moe_layer_t layer, int enabled);
 moe_status_t moe_layer_phase_times(moe_layer_t layer, const char** names, float* ms,
                                    uint32_t capacity, uint32_t* count);
+
+/* Peer-wait limit of the NVLink exchange (default MOE_P2P_TIMEOUT_S or 600 s;
+ * 0 = wait forever, like NCCL).  A peer that misses it does not kill the
+ * context: the waits record an error code, later waits return at once, and
+ * moe_layer_comm_status reports it (MOE_ERR_NCCL, "layer.exchange: peer p did
+ * not signal slot s ...").  comm_status synchronises with the device. */
+moe_status_t moe_layer_set_peer_timeout(moe_layer_t layer, double seconds);
+moe_status_t moe_layer_comm_status(moe_layer_t layer, int32_t* code);
 
 /* ----------------------------------------------------------------------
  * EP communicator (NCCL over NVLink): the unique id is exchanged by the host

@@ -229,6 +229,8 @@ SIGNATURES = {
     "moe_layer_train_step_host": (_I, [_VP, C.POINTER(LayerParams), _VP, _VP, _F, _VP, _VP,
                                        C.POINTER(LayerGrads), _VP]),
     "moe_layer_set_profiling": (_I, [_VP, _I]),
+    "moe_layer_set_peer_timeout": (_I, [_VP, C.c_double]),
+    "moe_layer_comm_status": (_I, [_VP, C.POINTER(C.c_int32)]),
     "moe_layer_phase_times": (_I, [_VP, C.POINTER(C.c_char_p), C.POINTER(_F), _U32,
                                    C.POINTER(_U32)]),
     "moe_comm_unique_id": (_I, [_VP]),

@@ -460,6 +460,26 @@ moe_status_t moe_layer_set_profiling(moe_layer_t layer, int enabled) {
   });
 }
 
+moe_status_t moe_layer_set_peer_timeout(moe_layer_t layer, double seconds) {
+  return guard([&] {
+    moe::arg_check(layer != nullptr, "peer_timeout: layer must be non-null");
+    moe::config_check(seconds >= 0.0, "layer.peer_timeout: must be >= 0 (0 = wait forever)");
+    reinterpret_cast<moe::Layer*>(layer)->win.timeout_ns = (uint64_t)(seconds * 1e9);
+  });
+}
+
+moe_status_t moe_layer_comm_status(moe_layer_t layer, int32_t* code) {
+  return guard([&] {
+    moe::arg_check(layer != nullptr && code != nullptr, "comm_status: null argument");
+    auto* L = reinterpret_cast<moe::Layer*>(layer);
+    *code = L->p2p ? moe::p2p_status(L->win) : 0;
+    if (*code != 0)
+      moe::fail(MOE_ERR_NCCL, "layer.exchange: peer " + std::to_string((*code - 1000) % 16) +
+                                  " did not signal slot " + std::to_string((*code - 1000) / 16) +
+                                  " within the peer timeout");
+  });
+}
+
 moe_status_t moe_layer_phase_times(moe_layer_t layer, const char** names, float* ms,
                                    uint32_t capacity, uint32_t* count) {
   return guard([&] {

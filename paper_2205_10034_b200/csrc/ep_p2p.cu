@@ -17,10 +17,13 @@
 // ld.acquire.sys in a one-block wait kernel.  Reuse safety: a phase (forward or
 // backward) starts only after every peer has finished its previous phase
 // (SLOT_PHASE), which is when it last read the buffers this phase overwrites.
-// Spins time out after 30 s with __trap() rather than hanging the device.
+// Spins time out after a configurable limit (MOE_P2P_TIMEOUT_S, default 600 s,
+// 0 = never) by recording an error code instead of trapping; teardown is a
+// flag handshake so no peer store can land in a freed window.
 //
 // Receive order follows alltoall_flat (collectives.cpp:10-21): sources in rank
 // order inside every expert region.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -81,16 +84,23 @@ __device__ void grid_done_signal(const Win& w, uint32_t* ctr, int slot, uint64_t
   }
 }
 
+// Spin until every peer's flag reaches `target`.  timeout_ns == 0 waits
+// forever (NCCL's behaviour); otherwise a late peer sets *err = 1000 +
+// 16*slot + peer and the wait gives up WITHOUT trapping, so the context
+// survives and the host can read the code (moe_layer_comm_status) and recover
+// or abort.  Once *err is set every later wait returns at once (fail fast).
 __global__ void p2p_wait_kernel(const uint64_t* flags, uint32_t P, uint32_t me, int slot,
-                                uint64_t target, int32_t* err) {
+                                uint64_t target, int32_t* err, uint64_t timeout_ns) {
   const uint32_t p = threadIdx.x;
   if (p < P && p != me) {
     const uint64_t* f = flags + (uint64_t)slot * P + p;
     const uint64_t t0 = globaltimer();
+    volatile int32_t* verr = err;
     while (ld_acquire_sys(f) < target) {
-      if (globaltimer() - t0 > 30000000000ull) {
-        atomicExch(err, 1000 + slot * 16 + (int)p);
-        __trap();
+      if (*verr != 0) break;
+      if (timeout_ns && globaltimer() - t0 > timeout_ns) {
+        atomicCAS(err, 0, 1000 + slot * 16 + (int)p);
+        break;
       }
       __nanosleep(64);
     }
@@ -363,6 +373,12 @@ uint32_t* ctr_of(const P2PWindow& w, int i) {
       ::moe::fail(MOE_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));  \
   } while (0)
 
+uint64_t p2p_default_timeout_ns() {
+  const char* v = std::getenv("MOE_P2P_TIMEOUT_S");
+  const double s = v && *v ? std::atof(v) : 600.0;
+  return s <= 0 ? 0 : (uint64_t)(s * 1e9);
+}
+
 void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t E, uint64_t Cs,
                uint64_t row_bytes, uint64_t n_red, cudaStream_t st) {
   config_check(P <= 8, "layer.ep_size: P2P exchange supports up to 8 GPUs of one box");
@@ -376,6 +392,7 @@ void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t 
   w.Rmax = (uint64_t)P * Cs;
   w.row_bytes = row_bytes;
   w.n_red = (n_red + 3) / 4 * 4;
+  w.timeout_ns = p2p_default_timeout_ns();
   const uint64_t region = (uint64_t)w.El * w.Rmax * row_bytes;  // == E * Cs rows
   const uint64_t home = (uint64_t)E * Cs * row_bytes;
   w.off_xr = 0;
@@ -420,7 +437,29 @@ void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t 
   MOE_CUDA(cudaFree(one));
 }
 
+int32_t p2p_status(const P2PWindow& w) {
+  if (!w.err) return 0;
+  int32_t e = 0;
+  MOE_CUDA(cudaMemcpy(&e, w.err, 4, cudaMemcpyDeviceToHost));
+  return e;
+}
+
 void p2p_teardown(P2PWindow& w) {
+  if (w.P > 1 && w.base) {
+    // Handshake before unmapping: after this rank's device work is done it
+    // stores BYE into every peer's window (its last store into any of them)
+    // and waits for every peer's BYE in its own.  Once all have arrived no
+    // peer will write here again, so the window can be freed.
+    cudaStream_t st = nullptr;
+    if (cudaDeviceSynchronize() == cudaSuccess &&
+        cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess) {
+      p2p_signal_kernel<<<1, 32, 0, st>>>(win_of(w), SLOT_BYE, 1);
+      p2p_wait_kernel<<<1, 32, 0, st>>>(reinterpret_cast<const uint64_t*>(w.base + w.off_flags),
+                                         w.P, w.me, SLOT_BYE, 1, w.err, w.timeout_ns);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  }
   for (uint32_t p = 0; p < w.P; ++p)
     if (p != w.me && w.peer_host[p]) cudaIpcCloseMemHandle(w.peer_host[p]);
   if (w.peer_dev) cudaFree(w.peer_dev);
@@ -432,7 +471,7 @@ void p2p_teardown(P2PWindow& w) {
 void p2p_wait(const P2PWindow& w, int slot, uint64_t target, cudaStream_t st) {
   if (w.P <= 1) return;
   p2p_wait_kernel<<<1, 32, 0, st>>>(reinterpret_cast<const uint64_t*>(w.base + w.off_flags), w.P,
-                                     w.me, slot, target, w.err);
+                                     w.me, slot, target, w.err, w.timeout_ns);
   MOE_LAUNCH_CHECK("p2p_wait_kernel");
   count_launch();
 }

@@ -18,7 +18,8 @@ enum P2PSlot : int {
   SLOT_DY = 4,        // src's g*dy rows are in our recv_dy
   SLOT_DX = 5,        // src pushed our dX rows into our home dX
   SLOT_GRAD = 6,      // src's replicated-gradient partials are in our red[src]
-  NSLOT = 7
+  SLOT_BYE = 7,       // src has finished all work and will not write here again
+  NSLOT = 8
 };
 
 // One cudaMalloc per rank holding everything peers write into; mapped into
@@ -41,14 +42,18 @@ struct P2PWindow {
   uint8_t* peer_host[8] = {};
   uint8_t** peer_dev = nullptr;
   int32_t* err = nullptr;
+  uint64_t timeout_ns = 0;  // peer-wait limit, 0 = wait forever
 };
 
 void p2p_setup(P2PWindow& w, void* nccl_comm, uint32_t P, uint32_t me, uint32_t E, uint64_t Cs,
                uint64_t row_bytes, uint64_t n_red, cudaStream_t st);
 void p2p_teardown(P2PWindow& w);
+// Device error code of the peer waits (0 = ok, 1000 + 16*slot + peer = that
+// peer timed out); synchronous read.
+int32_t p2p_status(const P2PWindow& w);
 
-// Wait until flags[slot][src] >= target for every src != me (device spin with
-// a timeout that traps instead of hanging the GPU).
+// Wait until flags[slot][src] >= target for every src != me (device spin;
+// after w.timeout_ns it records an error code and gives up instead of hanging).
 void p2p_wait(const P2PWindow& w, int slot, uint64_t target, cudaStream_t st);
 // Write `value` into every peer's flags[slot][me] (after all prior work on st).
 void p2p_signal(const P2PWindow& w, int slot, uint64_t value, cudaStream_t st);

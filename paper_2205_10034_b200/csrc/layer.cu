@@ -193,10 +193,7 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
 }
 
 Layer::~Layer() {
-  if (p2p) {
-    cudaDeviceSynchronize();
-    p2p_teardown(win);
-  }
+  if (p2p) p2p_teardown(win);  // device sync + BYE handshake, then unmap / free
   for (int i = 0; i < kMaxPhases + 1; ++i) cudaEventDestroy(ev[i]);
   for (void* p : owned) cudaFree(p);
   if (x_stage) {
@@ -205,6 +202,7 @@ Layer::~Layer() {
     for (int i = 0; i < 3; ++i) cudaStreamDestroy(hp_stream[i]);
     for (int bb = 0; bb < 2; ++bb)
       for (int i = 0; i < 5; ++i) cudaEventDestroy(hp_ev[bb][i]);
+    cudaEventDestroy(hp_entry);
   }
 }
 
@@ -602,12 +600,18 @@ void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, con
     for (int b = 0; b < 2; ++b)
       for (int i = 0; i < 5; ++i)
         MOE_CUDA(cudaEventCreateWithFlags(&hp_ev[b][i], cudaEventDisableTiming));
+    MOE_CUDA(cudaEventCreateWithFlags(&hp_entry, cudaEventDisableTiming));
     // the first step's copies must not start before work already queued on st
-    MOE_CUDA(cudaEventRecord(hp_ev[0][4], st));
-    MOE_CUDA(cudaStreamWaitEvent(hp_stream[0], hp_ev[0][4], 0));
-    MOE_CUDA(cudaStreamWaitEvent(hp_stream[1], hp_ev[0][4], 0));
+    MOE_CUDA(cudaEventRecord(hp_entry, st));
+    MOE_CUDA(cudaStreamWaitEvent(hp_stream[0], hp_entry, 0));
   }
   cudaStream_t h2d = hp_stream[0], comp = hp_stream[1], d2h = hp_stream[2];
+  // Every call: the compute stream waits for whatever the caller queued on st
+  // since the last call (an optimizer step writing params, a consumer reading
+  // the gradients this step's backward overwrites).  The copy-in stream does
+  // not: it only reads the caller's host buffers and writes private staging.
+  MOE_CUDA(cudaEventRecord(hp_entry, st));
+  MOE_CUDA(cudaStreamWaitEvent(comp, hp_entry, 0));
   const int b = (int)(hp_iter & 1);
   cudaEvent_t* ev_b = hp_ev[b];
   uint8_t* base = static_cast<uint8_t*>(x_stage) + (uint64_t)b * 4 * bytes;

@@ -83,6 +83,7 @@ struct Layer {
   cudaStream_t hp_stream[3] = {};   // h2d, compute, d2h
   // per stage: x landed, dy landed, forward done, backward done, d2h done
   cudaEvent_t hp_ev[2][5] = {};
+  cudaEvent_t hp_entry = nullptr;   // caller-stream state at each train_step_host entry
   uint64_t hp_iter = 0;
   bool has_forward = false;
   // profiling

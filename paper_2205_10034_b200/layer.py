@@ -253,6 +253,16 @@ class MoELayer:
              dy_host.data_ptr(), float(d_aux), y_host.data_ptr(), dx_host.data_ptr(),
              C.byref(lg), _stream(stream))
 
+    def set_peer_timeout(self, seconds: float) -> None:
+        """Limit of the NVLink exchange's peer waits (0 = wait forever)."""
+        call("moe_layer_set_peer_timeout", self._h, float(seconds))
+
+    def comm_status(self) -> int:
+        """0, or raises MoEError when a peer missed the peer-wait limit."""
+        code = C.c_int32(0)
+        call("moe_layer_comm_status", self._h, C.byref(code))
+        return code.value
+
     def set_profiling(self, on: bool) -> None:
         call("moe_layer_set_profiling", self._h, 1 if on else 0)
 

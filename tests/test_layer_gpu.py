@@ -234,6 +234,47 @@ def test_train_step_host_pipeline_matches_device_calls():
     assert err < 1e-5
 
 
+def test_train_step_host_sees_param_updates_between_calls():
+    """an SGD update queued on the caller's stream between
+    train_step_host calls must be visible to the next step's forward, and must
+    not race its backward's gradient writes."""
+    cfg = MoEConfig(16, 2, 256, 512, 1.25, 2048, torch.bfloat16)
+    xs, dys = [], []
+
+    def sgd(layer):
+        p, g = layer.params, layer.grads
+        for n, gn in (("w1", "dw1"), ("w2", "dw2"), ("wg", "dwg"), ("b1", "db1")):
+            p[n].sub_((0.5 * g[gn]).to(p[n].dtype))
+
+    ref_layer = MoELayer(cfg)
+    ref_layer.init_params(5)
+    for i in range(4):
+        xs.append(ref_layer.make_input(300 + i))
+        dys.append(ref_layer.make_input(400 + i, T_DY))
+    ref = []
+    for x, dy in zip(xs, dys):
+        y = ref_layer.forward(x)
+        dx = ref_layer.backward(dy, d_aux=0.01)
+        ref.append((y.cpu(), dx.cpu()))
+        sgd(ref_layer)
+    torch.cuda.synchronize()
+    layer = MoELayer(cfg)
+    layer.init_params(5)
+    hx = [x.cpu().pin_memory() for x in xs]
+    hdy = [d.cpu().pin_memory() for d in dys]
+    hy = [torch.empty_like(h).pin_memory() for h in hx]
+    hdx = [torch.empty_like(h).pin_memory() for h in hx]
+    for i in range(4):
+        layer.train_step_host(hx[i], hdy[i], hy[i], hdx[i], d_aux=0.01)
+        sgd(layer)  # queued on the current stream, no host sync
+    torch.cuda.current_stream().synchronize()
+    for i in range(4):
+        assert torch.equal(hy[i], ref[i][0]), i
+        assert torch.equal(hdx[i], ref[i][1]), i
+    for n in ("w1", "w2", "wg"):
+        assert torch.equal(layer.params[n], ref_layer.params[n]), n
+
+
 def test_gradient_buckets_single_rank_scale():
     """moe_grad_buckets on one rank (no communicator): flushes follow the
     reverse-layer registration; only the scale is applied."""
@@ -275,3 +316,9 @@ def test_layer_empty_batch(dtype):
     assert y.shape == (0, 128) and dx.shape == (0, 128)
     for n, gr in layer.grads.items():
         assert not gr.abs().sum().item(), n
+
+
+def test_layer_fp32_c1_full_size_vs_oracle():
+    """config c1 exactly (T=4096, E=8, top-2, d=512, d_ff=2048, cf=1.25, fp32)
+    against the fp64 oracle at 1e-5 (c1 was only tested at T=512)."""
+    check_case(E=8, k=2, d=512, dff=2048, T=4096, cf=1.25, dtype=torch.float32, seed=2205)
