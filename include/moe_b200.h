@@ -215,10 +215,14 @@ typedef struct moe_gemm_problem {
   uint64_t ldb;           /* B row stride in elements (0: natural) */
   uint64_t b_rows;        /* rows allocated in B (0: num_b * (N or K), RAGGED_K: a_rows) */
   uint64_t c_rows;        /* rows allocated in C (0: a_rows for RAGGED_M)                */
-  float* colsum;          /* DGELU: [num_b][N] fp32 accumulated column sums, or NULL     */
+  float* colsum;          /* DGELU: [num_b][N] fp32 column sums of the stored C (written,
+                             not accumulated; fixed summation order: bitwise reproducible),
+                             or NULL                                                    */
   const void* gather_src; /* GATHER_ADD: [*, N] rows in dtype_c                          */
   const int32_t* gather_idx; /* GATHER_ADD: [rows][gather_k] row indices or -1          */
   uint32_t gather_k;
+  float* colsum_ws;       /* DGELU with colsum: partials [groups][ceil(colsum_max_m/32)][N] */
+  uint64_t colsum_max_m;  /* DGELU with colsum: upper bound of m[g] over the groups      */
 } moe_gemm_problem_t;
 
 moe_status_t moe_grouped_gemm(const moe_gemm_problem_t* problem, void* stream);
@@ -318,6 +322,20 @@ moe_status_t moe_layer_train_step_host(moe_layer_t layer, const moe_layer_params
                                        const void* x_host, const void* dy_host, float d_aux,
                                        void* y_host, void* dx_host, const moe_layer_grads_t* grads,
                                        void* stream);
+
+/* The same step with deferred outputs (the pipelined training loop): when
+ * `stream` reaches this call the gradients are final and params may be
+ * updated on `stream`, the host input buffers may be reused, and y_host /
+ * dx_host of the PREVIOUS call are complete; this call's y_host / dx_host are
+ * complete once `stream` reaches the next call or moe_layer_host_sync.  Lets
+ * the copy-out of step i overlap the compute of step i+1 although the caller
+ * queues work (an optimizer step) on `stream` between calls. */
+moe_status_t moe_layer_train_step_host_async(moe_layer_t layer, const moe_layer_params_t* params,
+                                             const void* x_host, const void* dy_host, float d_aux,
+                                             void* y_host, void* dx_host,
+                                             const moe_layer_grads_t* grads, void* stream);
+/* Make `stream` wait for every outstanding copy-out of train_step_host_async. */
+moe_status_t moe_layer_host_sync(moe_layer_t layer, void* stream);
 
 /* Per-phase device timings (ms) of the last forward/backward when profiling is
  * enabled with moe_layer_set_profiling(layer, 1): names/values as parallel

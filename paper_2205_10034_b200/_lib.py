@@ -115,6 +115,8 @@ class GemmProblem(C.Structure):
         ("gather_src", C.c_void_p),
         ("gather_idx", C.c_void_p),
         ("gather_k", C.c_uint32),
+        ("colsum_ws", C.c_void_p),
+        ("colsum_max_m", C.c_uint64),
     ]
 
 
@@ -228,6 +230,9 @@ SIGNATURES = {
                                 C.POINTER(LayerGrads), _VP]),
     "moe_layer_train_step_host": (_I, [_VP, C.POINTER(LayerParams), _VP, _VP, _F, _VP, _VP,
                                        C.POINTER(LayerGrads), _VP]),
+    "moe_layer_train_step_host_async": (_I, [_VP, C.POINTER(LayerParams), _VP, _VP, _F, _VP,
+                                             _VP, C.POINTER(LayerGrads), _VP]),
+    "moe_layer_host_sync": (_I, [_VP, _VP]),
     "moe_layer_set_profiling": (_I, [_VP, _I]),
     "moe_layer_set_peer_timeout": (_I, [_VP, C.c_double]),
     "moe_layer_comm_status": (_I, [_VP, C.POINTER(C.c_int32)]),

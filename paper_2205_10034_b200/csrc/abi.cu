@@ -453,6 +453,25 @@ moe_status_t moe_layer_train_step_host(moe_layer_t layer, const moe_layer_params
   });
 }
 
+moe_status_t moe_layer_train_step_host_async(moe_layer_t layer, const moe_layer_params_t* params,
+                                             const void* x_host, const void* dy_host, float d_aux,
+                                             void* y_host, void* dx_host,
+                                             const moe_layer_grads_t* grads, void* stream) {
+  return guard([&] {
+    moe::arg_check(layer != nullptr && params != nullptr && grads != nullptr,
+                   "train_step: layer/params/grads must be non-null");
+    reinterpret_cast<moe::Layer*>(layer)->train_step_host(*params, x_host, dy_host, d_aux, y_host,
+                                                          dx_host, *grads, S(stream), true);
+  });
+}
+
+moe_status_t moe_layer_host_sync(moe_layer_t layer, void* stream) {
+  return guard([&] {
+    moe::arg_check(layer != nullptr, "host_sync: layer must be non-null");
+    reinterpret_cast<moe::Layer*>(layer)->host_sync(S(stream));
+  });
+}
+
 moe_status_t moe_layer_set_profiling(moe_layer_t layer, int enabled) {
   return guard([&] {
     moe::arg_check(layer != nullptr, "profiling: layer must be non-null");

@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(GT) gate_logits_f32_kernel(uint64_t T, int d, 
 }
 
 // Block: TOKC tokens x 64 columns; thread (col = tid % 64, eg = tid / 64)
-// accumulates experts e = eg + 4 j over the chunk, then one atomic per output.
+// accumulates experts e = eg + 4 j over the chunk and stores the chunk's
+// partial; the chunks are summed in order afterwards (deterministic).
 constexpr int TOKC = 128;
 template <int NE>
 __global__ void __launch_bounds__(GT) gate_wgrad_f32_kernel(uint64_t T, int d, int E,
@@ -95,9 +96,11 @@ __global__ void __launch_bounds__(GT) gate_wgrad_f32_kernel(uint64_t T, int d, i
     for (int j = 0; j < NE; ++j)
       if (j < ne) acc[j] = fmaf(dr[4 * j], xv, acc[j]);
   }
+  // this token chunk's partial (summed over chunks in order by sum_parts)
+  float* const part = dwg + (uint64_t)blockIdx.x * E * d;
 #pragma unroll
   for (int j = 0; j < NE; ++j)
-    if (j < ne) atomicAdd(dwg + (uint64_t)(eg + 4 * j) * d + col, acc[j]);
+    if (j < ne) part[(uint64_t)(eg + 4 * j) * d + col] = acc[j];
 }
 
 // Block: 32 tokens x 64 columns; thread (col = tid % 64, tg = tid / 64)
@@ -167,16 +170,19 @@ void gate_logits_f32(uint64_t T, uint32_t d, uint32_t E, const float* x, const f
 }
 
 void gate_wgrad_f32(uint64_t T, uint32_t d, uint32_t E, const float* dl, const float* x,
-                    float* dwg, cudaStream_t st) {
-  MOE_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * E * d, st));
-  if (!T) return;
+                    float* dwg, float* ws, cudaStream_t st) {
+  if (!T) {
+    MOE_CUDA(cudaMemsetAsync(dwg, 0, sizeof(float) * E * d, st));
+    return;
+  }
+  arg_check(ws != nullptr, "gate_wgrad_f32.ws: workspace required");
   arg_check(E >= 1 && E <= 256, "gate_wgrad_f32: E must be in [1, 256]");
   const size_t smem = sizeof(float) * TOKC * E;
   dim3 grid((unsigned)ceil_div(T, TOKC), (unsigned)ceil_div(d, 64));
   auto go = [&](auto kern) {
     if (smem > 48 * 1024)
       MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    launch_pdl(kern, grid, GT, smem, st, T, (int)d, (int)E, dl, x, dwg);
+    launch_pdl(kern, grid, GT, smem, st, T, (int)d, (int)E, dl, x, ws);
   };
   const uint32_t ne = (E + 3) / 4;  // experts per thread
   if (ne <= 1) go(gate_wgrad_f32_kernel<1>);
@@ -188,6 +194,7 @@ void gate_wgrad_f32(uint64_t T, uint32_t d, uint32_t E, const float* dl, const f
   else go(gate_wgrad_f32_kernel<64>);
   MOE_LAUNCH_CHECK("gate_wgrad_f32_kernel");
   count_launch();
+  sum_parts(ws, (uint32_t)ceil_div(T, (uint64_t)TOKC), (uint64_t)E * d, E, d, d, false, dwg, st);
 }
 
 void gate_dx_f32(uint64_t T, uint32_t d, uint32_t E, uint32_t k, const float* dl, const float* wg,

@@ -32,7 +32,8 @@ struct Args {
   const float* bias;
   long long lda, ldb, ldc;
   long long b_rows;
-  float* colsum;
+  float* colsum;  // DGELU: per-tile partials [groups][cs_maxch][N] (reduced by seg_colsum)
+  int cs_maxch;
   const float* gsrc;
   const int* gidx;
   int gk;
@@ -343,7 +344,8 @@ __global__ void __launch_bounds__(THREADS, SIMT_MINB) simt_gemm_kernel(const Arg
 #pragma unroll
         for (int w8 = 0; w8 < THREADS / 32; ++w8) s += red[w8 * BN + tid];
         const int n = nb * BN + tid;
-        if (n < a.N) atomicAdd(a.colsum + (long long)bidx * a.N + n, s);
+        // the tile's 128-row block of group g owns this partial row
+        if (n < a.N) a.colsum[((long long)g * a.cs_maxch + mb) * a.N + n] = s;
       }
       __syncthreads();  // red aliases As: next tile's stash waits for the readers
     }
@@ -392,7 +394,10 @@ void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
   a.C2 = static_cast<float*>(p.C2);
   a.aux = static_cast<const float*>(p.aux);
   a.bias = p.bias;
-  a.colsum = p.colsum;
+  arg_check(p.epilogue != MOE_EPI_DGELU || !p.colsum || (p.colsum_ws && p.colsum_max_m >= 1),
+            "gemm.colsum_ws: DGELU column sums need colsum_ws / colsum_max_m");
+  a.colsum = p.epilogue == MOE_EPI_DGELU && p.colsum ? p.colsum_ws : nullptr;
+  a.cs_maxch = (int)((p.colsum_max_m + 31) / 32);
   a.gsrc = static_cast<const float*>(p.gather_src);
   a.gidx = p.gather_idx;
   a.gk = (int)p.gather_k;
@@ -441,6 +446,9 @@ void simt_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st) {
   }
   MOE_LAUNCH_CHECK("simt_gemm_kernel");
   count_launch();
+  if (p.kind == MOE_GEMM_RAGGED_M && p.epilogue == MOE_EPI_DGELU && p.colsum)
+    seg_colsum(p.groups, p.m, p.b, p.num_b, p.N, BM, (uint32_t)a.cs_maxch, p.colsum_ws, p.colsum,
+               st);
 }
 
 }  // namespace moe

@@ -88,7 +88,8 @@ struct Args {
   void* C;
   void* C2;
   const float* bias;
-  float* colsum;
+  float* colsum;  // DGELU: per-warp partials [groups][cs_maxch][N] (reduced by seg_colsum)
+  int cs_maxch;
   const void* gsrc;
   const int* gidx;
   int gk;
@@ -747,9 +748,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           s.x += __shfl_xor_sync(0xffffffffu, s.x, 16);
           s.y += __shfl_xor_sync(0xffffffffu, s.y, 16);
-          float* cs = args.colsum + (long long)bidx * args.N + n0 + 2 * cp;
-          if (rp == 0 && 2 * (int)cp < ncols) atomicAdd(cs, s.x);
-          if (rp == 0 && 2 * (int)cp + 1 < ncols) atomicAdd(cs + 1, s.y);
+          // this warp's 32-row block of group g owns its partial row: plain
+          // stores, summed in block order afterwards (deterministic)
+          float* cs = args.colsum + ((long long)g * args.cs_maxch + row0 / 32) * args.N + n0 + 2 * cp;
+          if (rp == 0 && 2 * (int)cp < ncols) cs[0] = s.x;
+          if (rp == 0 && 2 * (int)cp + 1 < ncols) cs[1] = s.y;
         }
       }
       tc_fence_before();
@@ -876,7 +879,8 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   a.C = p.C;
   a.C2 = p.C2;
   a.bias = p.bias;
-  a.colsum = p.colsum;
+  a.colsum = p.colsum_ws;
+  a.cs_maxch = (int)((p.colsum_max_m + 31) / 32);
   a.gsrc = p.gather_src;
   a.gidx = p.gather_idx;
   a.gk = (int)p.gather_k;
@@ -971,10 +975,18 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st, const RemoteR
         arg_check(!bmn && !f32, "gemm.epilogue: GELU needs K-major B and bf16 C");
         launch<256, false, false, 0, MOE_EPI_GELU, false, 2>(p, st);
         return;
-      case MOE_EPI_DGELU:
+      case MOE_EPI_DGELU: {
         arg_check(bmn && !f32, "gemm.epilogue: DGELU needs MN-major B and bf16 C");
-        launch<256, false, true, 0, MOE_EPI_DGELU, false, 2>(p, st);
+        arg_check(!p.colsum || (p.colsum_ws && p.colsum_max_m >= 1),
+                  "gemm.colsum_ws: DGELU column sums need colsum_ws / colsum_max_m");
+        moe_gemm_problem_t q = p;
+        if (!p.colsum) q.colsum_ws = nullptr;
+        launch<256, false, true, 0, MOE_EPI_DGELU, false, 2>(q, st);
+        if (p.colsum)
+          seg_colsum(p.groups, p.m, p.b, p.num_b, p.N, 32, (uint32_t)((p.colsum_max_m + 31) / 32),
+                     p.colsum_ws, p.colsum, st);
         return;
+      }
       case MOE_EPI_GATHER_ADD:
         arg_check(bmn && !f32 && p.gather_src && p.gather_idx && p.gather_k >= 1 &&
                       p.gather_k <= 2,
@@ -996,6 +1008,10 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st, const RemoteR
     }
     arg_check(p.epilogue == MOE_EPI_STORE && !p.transpose_c,
               "gemm.epilogue: RAGGED_K supports STORE or ATOMIC_ADD");
+    if (p.N <= 64) {  // narrow outputs (the split-K gate wgrad: N = E padded to 64)
+      launch<64, true, true, 1, MOE_EPI_STORE, true>(p, st);
+      return;
+    }
     if (p.M % 256 == 0) launch<256, true, true, 1, MOE_EPI_STORE, true, 2>(p, st);
     else launch<256, true, true, 1, MOE_EPI_STORE, true, 1>(p, st);
   }

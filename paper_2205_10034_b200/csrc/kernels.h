@@ -64,7 +64,9 @@ void route_forward(uint64_t T, uint32_t E, uint32_t k, uint64_t C, const float* 
 void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, const int32_t* expert,
                     const float* gate, const uint8_t* keep, const int32_t* count1,
                     const float* dgate, float d_aux, float* dlogits_f32, void* dlogits_lp,
-                    moe_dtype_t lp_dtype, uint32_t ld, float* dbg, cudaStream_t st);
+                    moe_dtype_t lp_dtype, uint32_t ld, float* dbg, float* dbg_ws,
+                    cudaStream_t st);
+inline uint64_t route_dbg_ws_floats(uint64_t T, uint32_t E) { return ((T + 255) / 256) * E; }
 
 // K3: dispatch tokens into the slot buffer [E][C][d] (send layout: rank-major,
 // then local expert, then position).  slot[t*k+i] = e*C+pos or -1.
@@ -89,7 +91,10 @@ void combine_backward(uint64_t T, uint32_t d, uint32_t E, uint32_t k, uint64_t C
 void gate_logits_f32(uint64_t T, uint32_t d, uint32_t E, const float* x, const float* wg,
                      const float* bg, float* logits, cudaStream_t st);
 void gate_wgrad_f32(uint64_t T, uint32_t d, uint32_t E, const float* dl, const float* x,
-                    float* dwg, cudaStream_t st);
+                    float* dwg, float* ws, cudaStream_t st);
+inline uint64_t gate_wgrad_f32_ws_floats(uint64_t T, uint32_t d, uint32_t E) {
+  return ((T + 127) / 128) * (uint64_t)E * d;
+}
 void gate_dx_f32(uint64_t T, uint32_t d, uint32_t E, uint32_t k, const float* dl, const float* wg,
                  const float* dXe, const int32_t* slot, float* dx, cudaStream_t st);
 
@@ -108,6 +113,22 @@ void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const i
                   uint32_t num_b, uint32_t N, moe_dtype_t dt, const void* X, float* out,
                   cudaStream_t st, uint64_t max_rows, float* part_ws = nullptr,
                   int32_t* ticket = nullptr);
+
+// Fixed-order reductions (reduce.cu) replacing float atomics on the gradient
+// paths, so gradients are bitwise reproducible:
+//   sum_parts : out[r][c] (or out[c][r] when transpose) =
+//               sum_{p < nparts} part[p*part_stride + r*ldp + c], p ascending
+//   seg_colsum: out[b][n] = sum over groups g (ascending) with gb[g] == b of
+//               sum_{ch < ceil(gm[g]/chunk)} ws[(g*maxch + ch)*N + n]
+void sum_parts(const float* part, uint32_t nparts, uint64_t part_stride, uint64_t rows,
+               uint64_t cols, uint64_t ldp, bool transpose, float* out, cudaStream_t st);
+void seg_colsum(uint32_t groups, const int32_t* gm, const int32_t* gb, uint32_t num_b, uint32_t N,
+                uint32_t chunk, uint32_t maxch, const float* ws, float* out, cudaStream_t st);
+// Workspace of the DGELU column-sum epilogue (moe_gemm_problem_t.colsum_ws):
+// [groups][ceil(max_m / 32)][N] floats.
+inline uint64_t gemm_colsum_ws_floats(uint32_t groups, uint32_t N, uint64_t max_m) {
+  return (uint64_t)groups * ((max_m + 31) / 32) * N;
+}
 
 // Round-robin placement relabel (include/moe_b200.h): pexpert = pi(expert),
 // pkept[pi(e)] = kept[e], pi(e) = (e % P) * (E / P) + e / P.

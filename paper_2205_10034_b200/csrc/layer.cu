@@ -137,6 +137,9 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
     const uint64_t nt = colsum_ticket_ints(ngroups, dm);
     cs_ticket = dalloc<int32_t>(owned, nt);
     MOE_CUDA(cudaMemset(cs_ticket, 0, nt * sizeof(int32_t)));
+    // fixed-order reduction workspaces (deterministic gradients, reduce.cu)
+    db1_ws = dalloc<float>(owned, gemm_colsum_ws_floats(ngroups, dff, mr));
+    if (d.has_gate_bias) dbg_ws = dalloc<float>(owned, std::max<uint64_t>(1, route_dbg_ws_floats(T, E)));
   }
   gm = dalloc<int32_t>(owned, E);
   ga = dalloc<int32_t>(owned, E);
@@ -182,6 +185,9 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
       sa[s] = (int32_t)(s * split_rows);
       sm[s] = (int32_t)std::min<uint64_t>(split_rows, T - std::min<uint64_t>(T, s * split_rows));
     }
+    for (uint32_t q = 0; q < nsplit; ++q) sb[q] = (int32_t)q;  // split q -> its own partial
+    dwg_ws = dalloc<float>(owned, dt == MOE_DTYPE_BF16 ? (uint64_t)nsplit * dm * Epad
+                                                        : std::max<uint64_t>(1, gate_wgrad_f32_ws_floats(T, dm, E)));
     split_m = dalloc<int32_t>(owned, nsplit);
     split_a = dalloc<int32_t>(owned, nsplit);
     split_b = dalloc<int32_t>(owned, nsplit);
@@ -397,42 +403,43 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     combine_backward(T, dm, E, k, C, pad, dt, dy, Yh, slot, gate, dkept(), dYs, dgate, st);
   }
   mark("combine_bwd", st);
-  // K2^T: dlogits
-  if (desc.has_gate_bias && g.dbg) MOE_CUDA(cudaMemsetAsync(g.dbg, 0, E * 4, st));
+  // K2^T: dlogits (and dbg, summed over token blocks in a fixed order)
   route_backward(T, E, k, logits, expert, gate, keep, count1, dgate, d_aux, dl_f32, dl_lp,
                  dt == MOE_DTYPE_BF16 ? MOE_DTYPE_BF16 : MOE_DTYPE_F32,
-                 dt == MOE_DTYPE_BF16 ? Epad : E, desc.has_gate_bias ? g.dbg : nullptr, st);
+                 dt == MOE_DTYPE_BF16 ? Epad : E, desc.has_gate_bias ? g.dbg : nullptr, dbg_ws,
+                 st);
   mark("route_bwd", st);
   // gate weight gradient dwg = dlogits^T x (split-K): needs only local data,
   // so it runs while the dY rows of the peers are still arriving
   if (dt == MOE_DTYPE_F32) {
-    gate_wgrad_f32(T, dm, E, dl_f32, static_cast<const float*>(x_saved_ptr), g.dwg, st);
-  } else {
+    gate_wgrad_f32(T, dm, E, dl_f32, static_cast<const float*>(x_saved_ptr), g.dwg, dwg_ws, st);
+  } else if (!T) {
     MOE_CUDA(cudaMemsetAsync(g.dwg, 0, (uint64_t)E * dm * 4, st));
-  }
-  if (T && dt != MOE_DTYPE_F32) {
+  } else {
+    // split-K over token blocks: split q stores its [dm][Epad] partial, then
+    // the partials are summed in split order and transposed to [E][dm]
     moe_gemm_problem_t p;
     std::memset(&p, 0, sizeof(p));
     p.kind = MOE_GEMM_RAGGED_K;
-    p.epilogue = MOE_EPI_ATOMIC_ADD;
+    p.epilogue = MOE_EPI_STORE;
     p.dtype_ab = dt;
     p.dtype_c = MOE_DTYPE_F32;
-    p.transpose_c = 1;
     p.groups = nsplit;
     p.M = dm;
-    p.N = E;
+    p.N = Epad;
     p.a_rows = T;
     p.b_rows = T;
-    p.num_b = 1;
+    p.num_b = nsplit;
     p.m = split_m;
     p.a_row = split_a;
     p.b = split_b;
     p.A = x_saved_ptr;
-    p.B = dt == MOE_DTYPE_BF16 ? dl_lp : (const void*)dl_f32;
-    p.ldb = dt == MOE_DTYPE_BF16 ? Epad : E;
-    p.C = g.dwg;
-    p.ldc = dm;
+    p.B = dl_lp;
+    p.ldb = Epad;
+    p.C = dwg_ws;
+    p.ldc = Epad;
     grouped_gemm(p, st);
+    sum_parts(dwg_ws, nsplit, (uint64_t)dm * Epad, dm, E, Epad, true, g.dwg, st);
   }
   // the replicated gate gradients are final here: push them to the peers now
   // so the closing all-reduce only sums (no wait on a late peer's push)
@@ -485,8 +492,8 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, s);
   };
   // K5^T dgrad: dH = (dY W2) * gelu'(h) (stored by ffn1), db1 = column sums
-  // of dH fused into the same epilogue; dXe = dH W1
-  MOE_CUDA(cudaMemsetAsync(g.db1, 0, (uint64_t)El * dff * 4, st));
+  // of dH fused into the same epilogue (per-block partials, fixed-order sum);
+  // dXe = dH W1
   {
     moe_gemm_problem_t p = expert_problem();
     p.epilogue = MOE_EPI_DGELU;
@@ -498,6 +505,8 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.C = dH;
     p.aux = Gp;
     p.colsum = g.db1;
+    p.colsum_ws = db1_ws;
+    p.colsum_max_m = p2p ? (uint64_t)P * Cs : Cs;
     p.ldc = dff;
     grouped_gemm(p, st);
   }
@@ -582,7 +591,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
 
 void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, const void* dy_host,
                             float d_aux, void* y_host, void* dx_host, const moe_layer_grads_t& g,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool deferred) {
   // Three-stream pipeline over double-buffered staging: H2D of step i+1 and
   // D2H of step i-1 overlap the compute of step i (PCIe is full duplex and the
   // copy engines need no SMs).  Finer-grained than whole steps: the forward
@@ -636,8 +645,23 @@ void Layer::train_step_host(const moe_layer_params_t& w, const void* x_host, con
   MOE_CUDA(cudaStreamWaitEvent(d2h, ev_b[3], 0));
   MOE_CUDA(cudaMemcpyAsync(dx_host, dxd, bytes, cudaMemcpyDeviceToHost, d2h));
   MOE_CUDA(cudaEventRecord(ev_b[4], d2h));
-  MOE_CUDA(cudaStreamWaitEvent(st, ev_b[4], 0));
+  if (!deferred) {
+    MOE_CUDA(cudaStreamWaitEvent(st, ev_b[4], 0));
+  } else {
+    // Deferred outputs: st waits for this step's compute (gradients final,
+    // params free to update) and for the PREVIOUS step's copy-out, so the
+    // D2H of step i overlaps the compute of step i+1 even when the caller
+    // queues an optimizer step on st between calls.
+    MOE_CUDA(cudaStreamWaitEvent(st, ev_b[3], 0));
+    if (hp_iter >= 1) MOE_CUDA(cudaStreamWaitEvent(st, hp_ev[b ^ 1][4], 0));
+  }
   ++hp_iter;
+}
+
+void Layer::host_sync(cudaStream_t st) {
+  if (!x_stage || hp_iter == 0) return;
+  // the copy-out stream is in order: the last step's event covers all
+  MOE_CUDA(cudaStreamWaitEvent(st, hp_ev[(hp_iter - 1) & 1][4], 0));
 }
 
 // --------------------------------------------------------------- comm -----

@@ -27,7 +27,9 @@ struct Layer {
                 const moe_layer_grads_t& g, cudaStream_t st);
   void train_step_host(const moe_layer_params_t& w, const void* x_host, const void* dy_host,
                        float d_aux, void* y_host, void* dx_host, const moe_layer_grads_t& g,
-                       cudaStream_t st);
+                       cudaStream_t st, bool deferred = false);
+  // deferred-output mode: make st wait for every outstanding copy-out
+  void host_sync(cudaStream_t st);
 
   moe_gemm_problem_t expert_problem() const;
   RemoteRows remote_rows(uint64_t home_off) const;
@@ -68,6 +70,9 @@ struct Layer {
   const int32_t* dkept() const { return rr ? pkept : kept; }
   float* cs_part = nullptr;      // db2 chunk partials (group_colsum)
   int32_t* cs_ticket = nullptr;  // db2 chunk tickets, self re-arming
+  float* db1_ws = nullptr;       // db1 partials of the DGELU epilogue [groups][rows/32][dff]
+  float* dbg_ws = nullptr;       // dbg partials [token blocks][E]
+  float* dwg_ws = nullptr;       // dwg split-K partials [nsplit][dm][Epad] (fp32: [T/128][E][dm])
   void *Gp = nullptr, *Aact = nullptr, *Yl = nullptr, *Yh = nullptr;
   // backward buffers
   float* dgate = nullptr;

@@ -681,10 +681,10 @@ __global__ void __launch_bounds__(RT_THREADS) route_bwd_kernel(
         cs[warp][lane + 32 * q] = a;
       }
       __syncthreads();
-      if (tid < ne) {
+      if (tid < ne) {  // this block's partial row; summed over blocks in order (sum_parts)
         float a = 0.f;
         for (int w = 0; w < 8; ++w) a += cs[w][tid];
-        atomicAdd(&dbg[e0 + tid], a);
+        dbg[(uint64_t)blockIdx.x * E + e0 + tid] = a;
       }
     }
   }
@@ -706,7 +706,7 @@ __global__ void colsum_kernel(const int32_t* __restrict__ gm, const int32_t* __r
   const T* base = X + ((uint64_t)ga[g] + r0) * N + n;
   float s = 0.f;
   for (int r = r0; r < r1; ++r, base += N) s += (float)*base;
-  atomicAdd(out + (uint64_t)gb[g] * N + n, s);
+  out[((uint64_t)g * gridDim.y + blockIdx.y) * N + n] = s;  // chunk partial (seg_colsum)
 }
 
 // bf16, 8 columns per thread (16-byte loads), 64 rows per block, 8 rows in flight
@@ -742,9 +742,9 @@ __global__ void colsum_bf16x8_kernel(const int32_t* __restrict__ gm, const int32
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] += __bfloat162float(h[q]);
   }
-  float* o = out + (uint64_t)gb[g] * N + n;
+  float* o = out + ((uint64_t)g * gridDim.y + blockIdx.y) * N + n;  // chunk partial (seg_colsum)
 #pragma unroll
-  for (int q = 0; q < 8; ++q) atomicAdd(o + q, acc[q]);
+  for (int q = 0; q < 8; ++q) o[q] = acc[q];
 }
 
 // One group per output row (groups == num_b): a block per (group, 256-column
@@ -945,9 +945,15 @@ void gather_dx(uint64_t T, uint32_t d, uint32_t k, moe_dtype_t dt, const void* d
 void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, const int32_t* expert,
                     const float* gate, const uint8_t* keep, const int32_t* count1,
                     const float* dgate, float d_aux, float* dlogits_f32, void* dlogits_lp,
-                    moe_dtype_t lp_dtype, uint32_t ld, float* dbg, cudaStream_t st) {
-  if (!T) return;
+                    moe_dtype_t lp_dtype, uint32_t ld, float* dbg, float* dbg_ws,
+                    cudaStream_t st) {
+  if (!T) {
+    if (dbg) MOE_CUDA(cudaMemsetAsync(dbg, 0, sizeof(float) * E, st));
+    return;
+  }
   const unsigned blocks = (unsigned)ceil_div(T, CHUNK);
+  arg_check(!dbg || dbg_ws, "route_backward.dbg_ws: workspace required for the gate-bias gradient");
+  float* const dbg_part = dbg ? dbg_ws : nullptr;  // [blocks][E] partials
   MOE_CUDA(cudaFuncSetAttribute(route_bwd_kernel<__nv_bfloat16>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, SLAB_SMEM));
   MOE_CUDA(cudaFuncSetAttribute(route_bwd_kernel<float>,
@@ -955,17 +961,19 @@ void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, con
   if (dlogits_lp && lp_dtype == MOE_DTYPE_BF16)
     launch_pdl(route_bwd_kernel<__nv_bfloat16>, blocks, RT_THREADS, SLAB_SMEM, st, 
         T, (int)E, (int)k, logits, expert, gate, keep, count1, dgate, d_aux, dlogits_f32,
-        (__nv_bfloat16*)dlogits_lp, (int)ld, dbg);
+        (__nv_bfloat16*)dlogits_lp, (int)ld, dbg_part);
   else
     launch_pdl(route_bwd_kernel<float>, blocks, RT_THREADS, SLAB_SMEM, st, T, (int)E, (int)k, logits, expert, gate, keep,
                                                     count1, dgate, d_aux, dlogits_f32,
-                                                    (float*)dlogits_lp, (int)ld, dbg);
+                                                    (float*)dlogits_lp, (int)ld, dbg_part);
   MOE_LAUNCH_CHECK("route_bwd_kernel");
   count_launch();
+  if (dbg) sum_parts(dbg_part, blocks, E, 1, E, E, false, dbg, st);
 }
 
 uint64_t colsum_ws_floats(uint32_t groups, uint32_t N, uint64_t max_rows) {
-  return (uint64_t)groups * std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)CS_CHUNK)) * N;
+  // the finest chunking of any colsum path (64 rows, colsum_bf16x8_kernel)
+  return (uint64_t)groups * std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)64)) * N;
 }
 uint64_t colsum_ticket_ints(uint32_t groups, uint32_t N) {
   return (uint64_t)groups * ceil_div((uint64_t)N, (uint64_t)256);
@@ -984,20 +992,26 @@ void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const i
     count_launch();
     return;
   }
-  MOE_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (uint64_t)num_b * N, st));
-  if (dt == MOE_DTYPE_BF16 && N % 8 == 0) {
-    dim3 grid(groups, (unsigned)ceil_div(max_rows, 64), (unsigned)ceil_div(N / 8, 128));
-    launch_pdl(colsum_bf16x8_kernel, grid, 128, 0, st, gm, ga, gb, (int)N, (const __nv_bfloat16*)X, out);
+  // several groups per output (or fp32): chunk partials into part_ws, then a
+  // fixed-order segmented sum over (group, chunk) -- deterministic
+  arg_check(part_ws != nullptr, "colsum.part_ws: workspace required");
+  const uint32_t chunk = dt == MOE_DTYPE_BF16 && N % 8 == 0 ? 64 : 128;
+  const uint32_t maxch = (uint32_t)std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)chunk));
+  if (chunk == 64) {
+    dim3 grid(groups, maxch, (unsigned)ceil_div(N / 8, 128));
+    launch_pdl(colsum_bf16x8_kernel, grid, 128, 0, st, gm, ga, gb, (int)N, (const __nv_bfloat16*)X,
+               part_ws);
   } else {
-    dim3 grid(groups, (unsigned)ceil_div(max_rows, 128), (unsigned)ceil_div(N, 256));
+    dim3 grid(groups, maxch, (unsigned)ceil_div(N, 256));
     if (dt == MOE_DTYPE_BF16)
       launch_pdl(colsum_kernel<__nv_bfloat16>, grid, 256, 0, st, gm, ga, gb, (int)N,
-                                                         (const __nv_bfloat16*)X, out);
+                                                         (const __nv_bfloat16*)X, part_ws);
     else
-      launch_pdl(colsum_kernel<float>, grid, 256, 0, st, gm, ga, gb, (int)N, (const float*)X, out);
+      launch_pdl(colsum_kernel<float>, grid, 256, 0, st, gm, ga, gb, (int)N, (const float*)X, part_ws);
   }
   MOE_LAUNCH_CHECK("colsum_kernel");
   count_launch();
+  seg_colsum(groups, gm, gb, num_b, N, chunk, maxch, part_ws, out, st);
 }
 
 // Round-robin expert placement: physical expert id pi(e) = (e % P) * El + e / P

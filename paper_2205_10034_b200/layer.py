@@ -246,12 +246,18 @@ class MoELayer:
         return dx
 
     def train_step_host(self, x_host: torch.Tensor, dy_host: torch.Tensor, y_host: torch.Tensor,
-                        dx_host: torch.Tensor, d_aux: float = 0.0, stream=None) -> None:
-        """End-to-end step from pinned host buffers (H2D, fwd, bwd, D2H)."""
+                        dx_host: torch.Tensor, d_aux: float = 0.0, stream=None,
+                        deferred: bool = False) -> None:
+        """End-to-end step from pinned host buffers (H2D, fwd, bwd, D2H).
+        deferred=True: y_host / dx_host are complete once the stream reaches
+        the next call or host_sync() (moe_layer_train_step_host_async)."""
         lp, lg = self._params(), self._grads()
-        call("moe_layer_train_step_host", self._h, C.byref(lp), x_host.data_ptr(),
-             dy_host.data_ptr(), float(d_aux), y_host.data_ptr(), dx_host.data_ptr(),
-             C.byref(lg), _stream(stream))
+        fn = "moe_layer_train_step_host_async" if deferred else "moe_layer_train_step_host"
+        call(fn, self._h, C.byref(lp), x_host.data_ptr(), dy_host.data_ptr(), float(d_aux),
+             y_host.data_ptr(), dx_host.data_ptr(), C.byref(lg), _stream(stream))
+
+    def host_sync(self, stream=None) -> None:
+        call("moe_layer_host_sync", self._h, _stream(stream))
 
     def set_peer_timeout(self, seconds: float) -> None:
         """Limit of the NVLink exchange's peer waits (0 = wait forever)."""

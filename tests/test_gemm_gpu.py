@@ -58,9 +58,11 @@ def ragged_m_case(dtype, b_mn, epi, N=512, K=256, groups=(200, 0, 128, 37, 300),
     p.aux = aux.data_ptr()
     p.bias = bias_t.data_ptr() if bias_t is not None else None
     p.ldc = N
-    cs = torch.zeros(nb, N, device=dev) if colsum else None
+    cs = torch.full((nb, N), 5.0, device=dev) if colsum else None  # written, not accumulated
     if colsum:
+        ws = torch.empty(G * ((max(groups) + 31) // 32) * N, device=dev)
         p.colsum = cs.data_ptr()
+        p.colsum_ws, p.colsum_max_m = ws.data_ptr(), max(groups)
     if gather is not None:
         gsrc, gidx, gk = gather
         p.gather_src, p.gather_idx, p.gather_k = gsrc.data_ptr(), gidx.data_ptr(), gk

@@ -258,21 +258,26 @@ def test_train_step_host_sees_param_updates_between_calls():
         ref.append((y.cpu(), dx.cpu()))
         sgd(ref_layer)
     torch.cuda.synchronize()
-    layer = MoELayer(cfg)
-    layer.init_params(5)
     hx = [x.cpu().pin_memory() for x in xs]
     hdy = [d.cpu().pin_memory() for d in dys]
     hy = [torch.empty_like(h).pin_memory() for h in hx]
     hdx = [torch.empty_like(h).pin_memory() for h in hx]
-    for i in range(4):
-        layer.train_step_host(hx[i], hdy[i], hy[i], hdx[i], d_aux=0.01)
-        sgd(layer)  # queued on the current stream, no host sync
-    torch.cuda.current_stream().synchronize()
-    for i in range(4):
-        assert torch.equal(hy[i], ref[i][0]), i
-        assert torch.equal(hdx[i], ref[i][1]), i
-    for n in ("w1", "w2", "wg"):
-        assert torch.equal(layer.params[n], ref_layer.params[n]), n
+    for deferred in (False, True):
+        layer = MoELayer(cfg)
+        layer.init_params(5)
+        for h in hy + hdx:
+            h.zero_()
+        for i in range(4):
+            layer.train_step_host(hx[i], hdy[i], hy[i], hdx[i], d_aux=0.01, deferred=deferred)
+            sgd(layer)  # queued on the current stream, no host sync
+        if deferred:
+            layer.host_sync()
+        torch.cuda.current_stream().synchronize()
+        for i in range(4):
+            assert torch.equal(hy[i], ref[i][0]), (deferred, i)
+            assert torch.equal(hdx[i], ref[i][1]), (deferred, i)
+        for n in ("w1", "w2", "wg"):
+            assert torch.equal(layer.params[n], ref_layer.params[n]), (deferred, n)
 
 
 def test_gradient_buckets_single_rank_scale():
@@ -322,3 +327,28 @@ def test_layer_fp32_c1_full_size_vs_oracle():
     """config c1 exactly (T=4096, E=8, top-2, d=512, d_ff=2048, cf=1.25, fp32)
     against the fp64 oracle at 1e-5 (c1 was only tested at T=512)."""
     check_case(E=8, k=2, d=512, dff=2048, T=4096, cf=1.25, dtype=torch.float32, seed=2205)
+
+
+@pytest.mark.parametrize("dtype,E,k,d,dff,T", [
+    (torch.bfloat16, 64, 1, 1024, 4096, 16384),  # c2 widths (split-K dWg: 16 splits)
+    (torch.bfloat16, 32, 2, 256, 512, 5000),     # ragged T, top-2
+    (torch.float32, 8, 2, 512, 2048, 4096),      # config c1
+])
+def test_gradients_bitwise_deterministic(dtype, E, k, d, dff, T):
+    """no float atomics on the gradient paths -- two identical
+    steps give bitwise-identical dx, dwg, dbg, dw1, db1, dw2, db2."""
+    cfg = MoEConfig(E, k, d, dff, 1.25, T, dtype, gate_bias=True)
+    layer = MoELayer(cfg)
+    layer.init_params(11, gate_bias=torch.linspace(-1, 1, E, device="cuda"))
+    x = layer.make_input(11)
+    dy = layer.make_input(11, T_DY)
+    runs = []
+    for _ in range(3):
+        y = layer.forward(x)
+        dx = layer.backward(dy, d_aux=0.01)
+        torch.cuda.synchronize()
+        runs.append({"y": y.clone(), "dx": dx.clone(),
+                     **{n: t.clone() for n, t in layer.grads.items() if t is not None}})
+    for r in runs[1:]:
+        for n, t in runs[0].items():
+            assert torch.equal(t, r[n]), n
