@@ -249,6 +249,119 @@ def bind_to_gpu_numa(local):
     return None
 
 
+# ------------------------------------------------------ reference metrics --
+def ring_predicted(layers, slots, section_bytes, compute_ns, bw, lat_ns):
+    """The reference's ring model (ring_offload.cpp:52-106 on the FIFO streams
+    of sim_engine.cpp; transfer time topology.cpp:73-84) for the same plan,
+    fed with the measured per-layer compute: predicted makespan / stall."""
+    K = min(slots, layers)
+    c = lat_ns + -(-section_bytes * 10**9 // int(bw))
+    load_end = [0] * layers
+    h2d = comp = total = 0
+    for i in range(K):
+        h2d += c
+        load_end[i] = h2d
+    end = 0
+    for i in range(layers):
+        s0 = max(load_end[i], comp)
+        comp = s0 + compute_ns[i]
+        total += compute_ns[i]
+        if i + K < layers:
+            h2d = max(h2d, comp) + c
+            load_end[i + K] = h2d
+    end = max(comp, max(load_end))
+    return {"makespan_ms": end / 1e6, "stall_ms": (end - total) / 1e6}
+
+
+def ring_leg(args, dev, layers=4, slots=2, tokens=131072):
+    """Config c5 (ring-of-sections inference) reduced to N=4 layers so the
+    pinned sections (2.15 GB each) stay within the bench's time budget; the
+    reference's infer-sim metrics (report.cpp:172-187) measured on the CUDA-
+    event timeline beside the reference model's prediction for the same plan."""
+    import torch
+
+    from paper_2205_10034_b200 import MoEConfig, MoELayer
+    from paper_2205_10034_b200.ring import RingOfSections
+    t0 = time.time()
+    cfg = MoEConfig(8, 2, 4096, 16384, 1.25, tokens, torch.bfloat16)
+    layer = MoELayer(cfg, device=dev)
+    ring = RingOfSections(layer, layers, slots, seed=5)
+    x = layer.make_input(3)
+    ring.run(x)
+    torch.cuda.synchronize()
+    runs = []
+    for _ in range(3):
+        _, tl = ring.run(x)
+        torch.cuda.synchronize()
+        runs.append(tl)
+    tl = sorted(runs, key=lambda r: r["makespan_ms"])[1]
+    sec = tl["section_bytes"]
+    loads = [e - s for s, e in zip(tl["load_start"], tl["load_end"])]
+    comp_ns = [int(1e6 * (e - s)) for s, e in zip(tl["compute_start"], tl["compute_end"])]
+    load_ms = statistics.median(loads)
+    out = {
+        "config": f"c5 reduced: {layers} layers (of 12), K={tl['slots']} slots, E=8 top-2, "
+                  f"d=4096, d_ff=16384, bf16, {tokens} tokens per pass, sections in pinned host "
+                  "memory",
+        "makespan_ms": tl["makespan_ms"], "compute_total_ms": tl["compute_total_ms"],
+        "stall_ms": tl["makespan_ms"] - tl["compute_total_ms"],
+        "peak_gpu_bytes": tl["peak_gpu_bytes"], "baseline_gpu_bytes": tl["baseline_gpu_bytes"],
+        "memory_reduction": 1.0 - tl["peak_gpu_bytes"] / tl["baseline_gpu_bytes"],
+        "tokens_per_s": tokens / (tl["makespan_ms"] / 1e3),
+        "section_bytes": sec, "h2d_gbs": sec / load_ms / 1e6,
+        "predicted_ref_default_link": ring_predicted(layers, slots, sec, comp_ns, 25e9, 2000),
+        "predicted_measured_link": ring_predicted(layers, slots, sec, comp_ns,
+                                                  sec / load_ms * 1e3, 2000),
+        "note": "predicted_* = the reference's simulate() on this plan with the measured "
+                "compute times and PCIe at the reference default (25 GB/s, 2 us; "
+                "scenario.cpp:59) or the measured H2D rate",
+        "setup_s": time.time() - t0,
+    }
+    ring.close()
+    del ring, layer, x
+    torch.cuda.empty_cache()
+    return out
+
+
+def a2a_fusion_leg(ep, ws, rank, E, Cs, d, iters=10):
+    """Fusion communication (§4.2, lower_slice_transfer collectives.cpp:
+    250-267): the c-config's expert slices (Cs rows x d bf16 each, E/N per peer)
+    sent as ONE message per peer vs one per expert slice; device time, max over
+    ranks (report.cpp:240-252 metric names)."""
+    import torch
+    import torch.distributed as dist
+    El = max(1, E // ws)
+    slice_bytes = Cs * d * 2
+    per_peer = El * slice_bytes
+    send = torch.empty(ws * per_peer, dtype=torch.uint8, device="cuda").random_(0, 255)
+    recv = torch.empty_like(send)
+    stream = torch.cuda.current_stream()
+    res = {}
+    for fused in (True, False):
+        for _ in range(2):
+            ep.alltoall_packed(send, recv, per_peer, El, fused)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            ep.alltoall_packed(send, recv, per_peer, El, fused)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / iters], device="cuda")
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        res["fused_ms" if fused else "unfused_ms"] = float(ms.item())
+    out_bytes = per_peer * (ws - 1)
+    del send, recv
+    torch.cuda.empty_cache()
+    return {"slices_per_peer": El, "slice_bytes": slice_bytes, "bytes_out_per_gpu": out_bytes,
+            "fused_ms": res["fused_ms"], "unfused_ms": res["unfused_ms"],
+            "fused_gbs": out_bytes / res["fused_ms"] / 1e6,
+            "unfused_gbs": out_bytes / res["unfused_ms"] / 1e6,
+            "speedup": res["unfused_ms"] / res["fused_ms"],
+            "api": "moe_alltoall_packed (NCCL over NVLink)"}
+
+
 # ------------------------------------------------------------------ GPU arm --
 def main():
     _redirect_stdout()
@@ -261,6 +374,10 @@ def main():
     ap.add_argument("--tokens", type=int, default=0, help="override T (tokens per GPU)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ring", action="store_true",
+                    help="skip the reduced c5 ring-of-sections leg (N=1 only)")
+    ap.add_argument("--timeline", default="",
+                    help="write the profiled step's phase timeline as trace-event JSON here")
     ap.add_argument("--placement", default="round_robin", choices=["contiguous", "round_robin"],
                     help="expert placement over the N GPUs (include/moe_b200.h); round-robin "
                          "spreads a skewed gate's hot experts over the ranks (c3 N=4: 2.3x), "
@@ -337,12 +454,22 @@ def main():
     phase_tot = {}
     for _ in range(args.steps):
         layer.forward(x)
-        for n, v in layer.phase_times().items():
+        fwd_ph = layer.phase_list()
+        for n, v in fwd_ph:
             phase_tot["fwd." + n] = phase_tot.get("fwd." + n, 0.0) + v
         layer.backward(dy, d_aux=0.01)
-        for n, v in layer.phase_times().items():
+        bwd_ph = layer.phase_list()
+        for n, v in bwd_ph:
             phase_tot["bwd." + n] = phase_tot.get("bwd." + n, 0.0) + v
     layer.set_profiling(False)
+    if args.timeline and rank == 0:
+        # the last profiled step as the reference's trace-event JSON
+        # (trace_export.cpp:28-58; TaskRecord per phase on the launch stream)
+        from paper_2205_10034_b200 import moesim
+        tasks = moesim.layer_step_timeline([("fwd." + n, v) for n, v in fwd_ph] +
+                                           [("bwd." + n, v) for n, v in bwd_ph],
+                                           stream=f"rank{rank}.compute")
+        moesim.export_trace(tasks, args.timeline)
     barrier()
     t_ms = torch.tensor([ms], device=dev)
     if ws > 1:
@@ -360,8 +487,10 @@ def main():
     drop = 1.0 - kept_local / float(T * k)
     imb_ref = None
     if cfg.get("skew"):
-        import oracle  # reference statistic only (workload.cpp:19-66), not on the timed path
-        imb_ref = oracle.imbalance_ratio(oracle.gen_trace(7, 1, 1, E, T, cfg["skew"]))
+        # the reference's statistic of its own skewed trace (workload.cpp:19-66)
+        # through this package's drop-in gen_trace / imbalance_ratio (golden-pinned)
+        from paper_2205_10034_b200 import moesim
+        imb_ref = moesim.imbalance_ratio(moesim.gen_trace(7, 1, 1, E, T, cfg["skew"]))
 
     # ---- roofline of the dominant kernel (expert grouped GEMMs, tcgen05) ----
     pk = peaks()
@@ -497,6 +626,11 @@ def main():
                "sample": f"{n} tokens of the {args.config} layer fwd+bwd ({dt:.1f} s, "
                          "oracle/moe_oracle.c fp64-accumulate, OpenMP)"}
 
+    ring = None
+    if rank == 0 and ws == 1 and not args.no_ring and dtype == torch.bfloat16:
+        ring = ring_leg(args, dev)
+    a2a_fusion = a2a_fusion_leg(ep, ws, rank, E, layer.capacity, d) if ws > 1 else None
+
     a2a_ms = sum(v for n, v in phase_tot.items() if ".a2a" in n) / args.steps
     nvlink = None
     if ws > 1:
@@ -550,10 +684,12 @@ def main():
         "clocks": clocks,
         "routing": {"imbalance_ratio": imb, "drop_rate": drop,
                     "gen_trace_imbalance_ratio": imb_ref,
-                    "note": "imbalance over top-1 choices (max/mean count1); gen_trace_* = the "
-                            "reference's moesim_imbalance_ratio(gen_trace(7, 1, 1, E, T, skew))"
+                    "note": "imbalance over top-1 choices (max/mean count1); gen_trace_* = "
+                            "imbalance_ratio(gen_trace(7, 1, 1, E, T, skew)) of the reference's "
+                            "Zipf generator"
                             if imb_ref else "imbalance over top-1 choices (max/mean count1)"},
         "a2a_ms_per_step": a2a_ms if ws > 1 else 0.0,
+        "ring": ring, "a2a_fusion": a2a_fusion,
         "nvlink": nvlink,
         "phases_ms_per_step": {n: v / args.steps for n, v in sorted(phase_tot.items())},
     }

@@ -56,10 +56,12 @@ def ragged_m(G, rows, N, K, epi=0, b_mn=False, out_f32=False, colsum=True):
     p.m, p.a_row, p.c_row, p.b = m.data_ptr(), ar.data_ptr(), ar.data_ptr(), b.data_ptr()
     p.A, p.B, p.C, p.C2, p.aux = A.data_ptr(), B.data_ptr(), Cm.data_ptr(), C2.data_ptr(), aux.data_ptr()
     p.bias = bias.data_ptr() if epi in (0, 1) else None
+    ws = torch.empty(G * ((rows + 31) // 32) * N, device=dev)
     if epi == 2 and colsum:
         p.colsum = cs.data_ptr()
+        p.colsum_ws, p.colsum_max_m = ws.data_ptr(), rows
     p.ldc = N
-    keep = (A, B, Cm, C2, aux, bias, m, ar, b, cs)
+    keep = (A, B, Cm, C2, aux, bias, m, ar, b, cs, ws)
     return p, keep, 2.0 * G * rows * N * K
 
 
@@ -85,6 +87,8 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rows", type=int, default=1024)
     ap.add_argument("--groups", type=int, default=64)
+    ap.add_argument("--only", default="", help="comma-separated substrings of variant names")
+    ap.add_argument("--json", action="store_true")
     a = ap.parse_args()
     G, R, d, f = a.groups, a.rows, 1024, 4096
     variants = [
@@ -100,9 +104,15 @@ def main():
         ("wgrad2 shp  MN/MN    f32  STORE", lambda: ragged_k(G, R, f, d)),
     ]
     for name, mk in variants:
+        if a.only and not any(o in name for o in a.only.split(",")):
+            continue
         p, keep, flops = mk()
         ms = timed(lambda: grouped_gemm(p), a.reps)
-        print(f"{name}  {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TFLOP/s", flush=True)
+        if a.json:
+            import json
+            print(json.dumps({"name": name.strip(), "us": ms * 1e3}), flush=True)
+        else:
+            print(f"{name}  {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TFLOP/s", flush=True)
         del keep
 
 

@@ -3,6 +3,7 @@
 // /root/reference/proj/core/src by oracle/Makefile into oracle/_ref/.  Used to
 // pin oracle/moe_oracle.c and to generate tests/golden/ fixtures.  Never linked
 // by the product.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -16,7 +17,9 @@
 #include "moesim/prefetch_cache.hpp"
 #include "moesim/ring_offload.hpp"
 #include "moesim/rng.hpp"
+#include "moesim/sim_engine.hpp"
 #include "moesim/topology.hpp"
+#include "moesim/trace_export.hpp"
 #include "moesim/workload.hpp"
 
 using namespace moesim;
@@ -313,6 +316,50 @@ int ref_sparse_cache_run(uint64_t cpu_size, double threshold, double beta, uint3
     *snap_n = k;
     *acc = cache.acc_caches();
     *steps = cache.steps();
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+// trace_export.cpp:28-50 timeline_to_trace_json(...).dump() of a Timeline
+// built from n tasks (labels / streams as NUL-separated strings, start/end in
+// ns); validate_trace_json of the parsed text into err ("" = valid).
+int ref_timeline_trace_json(uint64_t n, const char* labels, const char* streams,
+                            const int64_t* start, const int64_t* end, char* out, uint64_t cap,
+                            uint64_t* len) {
+  try {
+    Timeline tl;
+    const char* lp = labels;
+    const char* sp = streams;
+    for (uint64_t i = 0; i < n; ++i) {
+      TaskRecord t;
+      t.id = i;
+      t.label = lp;
+      t.stream = sp;
+      lp += t.label.size() + 1;
+      sp += t.stream.size() + 1;
+      t.start = start[i];
+      t.end = end[i];
+      tl.streams[t.stream];
+      tl.makespan = std::max<TimeNs>(tl.makespan, t.end);
+      tl.tasks.push_back(std::move(t));
+    }
+    const std::string s = timeline_to_trace_json(tl).dump(2);
+    *len = s.size();
+    if (s.size() + 1 > cap) return 8;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  } catch (...) {
+    return code_of(std::current_exception());
+  }
+}
+
+int ref_validate_trace_json(const char* text, char* err, uint64_t err_cap) {
+  try {
+    const std::string e = validate_trace_json(nlohmann::json::parse(text));
+    std::strncpy(err, e.c_str(), err_cap - 1);
+    err[err_cap - 1] = 0;
     return 0;
   } catch (...) {
     return code_of(std::current_exception());

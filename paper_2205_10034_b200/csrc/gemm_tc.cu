@@ -43,7 +43,7 @@ constexpr int STG = 2048;  // one 32-row x 64B staging tile
 // CG = CTAs per MMA (cta_group): CG == 2 pairs two SMs on a 256 x BN tile,
 // each CTA holding its 128 A rows and BN/2 B columns (halves the per-SM smem
 // operand traffic of the 128 x 256 single-CTA MMA).
-template <int BN, int EPI, bool CF32, int CG>
+template <int BN, int EPI, bool CF32, int CG, int KIND = 0>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
@@ -57,9 +57,18 @@ struct Cfg {
   static constexpr int NAUX = (EPI == MOE_EPI_DGELU) ? 2 : (EPI == MOE_EPI_GATHER_ADD ? 8 : 0);
   // output staging buffers per warp: double-buffered (the TMA store of chunk c
   // drains while chunk c+1 is computed) where the epilogue is the long pole
-  static constexpr int NBUF = (EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU || CF32) ? 2 : 1;
+  // -- except the weight gradients (RAGGED_K): single-buffered, and no bias
+  // slice, so the freed shared memory buys a sixth operand stage for their
+  // MN-major loads (A/B on c2: wgrad 0.50 -> 0.45 ms; the MMA warp was waiting
+  // on operands, not on the epilogue)
+#ifndef MOE_WGRAD_NBUF
+#define MOE_WGRAD_NBUF 1
+#endif
+  static constexpr int NBUF = KIND == 1 && EPI == MOE_EPI_STORE ? MOE_WGRAD_NBUF
+                              : (EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU || CF32) ? 2 : 1;
   // + the warp's bias slice of the current tile (STORE/GELU): BN/2 floats
-  static constexpr int BIAS_BYTES = (EPI == MOE_EPI_STORE || EPI == MOE_EPI_GELU) ? BN * 2 : 0;
+  static constexpr int BIAS_BYTES =
+      KIND == 0 && (EPI == MOE_EPI_STORE || EPI == MOE_EPI_GELU) ? BN * 2 : 0;
   // staging tiles stay 2 KB aligned (the TMA swizzle follows address bits)
   static constexpr int WARP_EPI_BYTES = (NBUF * NOUT + NAUX) * STG;
   // as many operand stages as fit next to the epilogue buffers (<= 8)
@@ -194,7 +203,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
                    const __grid_constant__ CUtensorMap tmAux, const Args args,
                    const __grid_constant__ RemoteOut ro) {
-  using C_ = Cfg<BN, EPI, CF32, CG>;
+  using C_ = Cfg<BN, EPI, CF32, CG, KIND>;
   constexpr int TM = BM * CG;  // tile rows per work item (the CTA pair)
   const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // 0 = leader
   const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -823,7 +832,7 @@ template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32, int CG = 1
           bool REMOTE = false>
 static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
                    const RemoteRows* remote = nullptr) {
-  using C_ = Cfg<BN, EPI, CF32, CG>;
+  using C_ = Cfg<BN, EPI, CF32, CG, KIND>;
   constexpr int BH = BN / CG;
   auto kern = tc_gemm_kernel<BN, A_MN, B_MN, KIND, EPI, CF32, CG, REMOTE>;
   // the smem opt-in is per device: remember which devices were configured

@@ -7,16 +7,20 @@
 // gradients are bitwise reproducible run to run — the reference's simulator
 // is deterministic by construction (acceptance_main.cpp:442-486).
 //
-// Both kernels are HBM/L2-bound streaming reductions: one thread per output
-// element walks the partials in index order; adjacent threads read adjacent
-// columns (coalesced 128-byte lines per warp).
+// Both kernels are HBM/L2-bound streaming reductions: a warp reads 32
+// adjacent outputs of one partial (a coalesced 128-byte line), eight warps
+// split the partials and are combined in a fixed order.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace moe {
 namespace {
 
-constexpr int RT = 256;
+// Block = 32 output columns x PW part-groups: lane = column, warp w sums the
+// partials p = w, w + PW, ... (all its loads independent), then warp 0 adds
+// the PW group sums in order -- a fixed summation order, bitwise reproducible.
+constexpr int PW = 8;
+constexpr int RT = 32 * PW;
 
 // out[r*cols + c] (transpose: out[c*rows + r]) = sum_{p < nparts} part[p*pstride + r*ldp + c]
 __global__ void __launch_bounds__(RT) sum_parts_kernel(const float* __restrict__ part,
@@ -25,26 +29,28 @@ __global__ void __launch_bounds__(RT) sum_parts_kernel(const float* __restrict__
                                                        int transpose, float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  const uint64_t i = (uint64_t)blockIdx.x * RT + threadIdx.x;
-  if (i >= rows * cols) return;
-  const uint64_t r = i / cols, c = i % cols;
+  __shared__ float red[PW][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t i = (uint64_t)blockIdx.x * 32 + lane;
+  const bool ok = i < rows * cols;
+  const uint64_t r = ok ? i / cols : 0, c = ok ? i % cols : 0;
   const float* p = part + r * ldp + c;
   float s = 0.f;
-  uint32_t q = 0;
-  for (; q + 4 <= nparts; q += 4) {  // 4 loads in flight, summed in index order
-    const float a0 = __ldcg(p + (uint64_t)q * pstride), a1 = __ldcg(p + (uint64_t)(q + 1) * pstride);
-    const float a2 = __ldcg(p + (uint64_t)(q + 2) * pstride), a3 = __ldcg(p + (uint64_t)(q + 3) * pstride);
-    s += a0;
-    s += a1;
-    s += a2;
-    s += a3;
+  if (ok)
+    for (uint32_t q = w; q < nparts; q += PW) s += __ldcg(p + (uint64_t)q * pstride);
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && ok) {
+    float t = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < PW; ++k) t += red[k][lane];
+    out[transpose ? c * rows + r : i] = t;
   }
-  for (; q < nparts; ++q) s += __ldcg(p + (uint64_t)q * pstride);
-  out[transpose ? c * rows + r : i] = s;
 }
 
 // out[b][n] = sum over groups g (ascending) with gb[g] == b of
 //             sum over chunks ch < ceil(gm[g] / chunk) of ws[(g*maxch + ch)*N + n]
+// (chunks split over the PW warps like sum_parts)
 __global__ void __launch_bounds__(RT) seg_colsum_kernel(uint32_t groups, const int32_t* __restrict__ gm,
                                                         const int32_t* __restrict__ gb, uint32_t N,
                                                         uint32_t chunk, uint32_t maxch,
@@ -54,31 +60,31 @@ __global__ void __launch_bounds__(RT) seg_colsum_kernel(uint32_t groups, const i
   pdl_trigger();
   __shared__ int s_nch[1024];
   __shared__ int s_b[1024];
+  __shared__ float red[PW][32];
   const int b = blockIdx.x;
   for (uint32_t g = threadIdx.x; g < groups; g += RT) {
     s_b[g] = gb[g];
     s_nch[g] = min((int)maxch, (gm[g] + (int)chunk - 1) / (int)chunk);
   }
   __syncthreads();
-  const uint32_t n = blockIdx.y * RT + threadIdx.x;
-  if (n >= N) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t n = blockIdx.y * 32 + lane;
   float s = 0.f;
-  for (uint32_t g = 0; g < groups; ++g) {
-    if (s_b[g] != b) continue;
-    const float* p = ws + (uint64_t)g * maxch * N + n;
-    const int nch = s_nch[g];
-    int ch = 0;
-    for (; ch + 4 <= nch; ch += 4) {
-      const float a0 = __ldcg(p + (uint64_t)ch * N), a1 = __ldcg(p + (uint64_t)(ch + 1) * N);
-      const float a2 = __ldcg(p + (uint64_t)(ch + 2) * N), a3 = __ldcg(p + (uint64_t)(ch + 3) * N);
-      s += a0;
-      s += a1;
-      s += a2;
-      s += a3;
+  if (n < N) {
+    for (uint32_t g = 0; g < groups; ++g) {
+      if (s_b[g] != b) continue;
+      const float* p = ws + (uint64_t)g * maxch * N + n;
+      for (int ch = w; ch < s_nch[g]; ch += PW) s += __ldcg(p + (uint64_t)ch * N);
     }
-    for (; ch < nch; ++ch) s += __ldcg(p + (uint64_t)ch * N);
   }
-  out[(uint64_t)b * N + n] = s;
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && n < N) {
+    float t = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < PW; ++k) t += red[k][lane];
+    out[(uint64_t)b * N + n] = t;
+  }
 }
 
 }  // namespace
@@ -87,7 +93,7 @@ void sum_parts(const float* part, uint32_t nparts, uint64_t part_stride, uint64_
                uint64_t cols, uint64_t ldp, bool transpose, float* out, cudaStream_t st) {
   const uint64_t n = rows * cols;
   if (!n) return;
-  launch_pdl(sum_parts_kernel, (unsigned)ceil_div(n, (uint64_t)RT), RT, 0, st, part, nparts,
+  launch_pdl(sum_parts_kernel, (unsigned)ceil_div(n, (uint64_t)32), RT, 0, st, part, nparts,
              part_stride, rows, cols, ldp, transpose ? 1 : 0, out);
   MOE_LAUNCH_CHECK("sum_parts_kernel");
   count_launch();
@@ -97,7 +103,7 @@ void seg_colsum(uint32_t groups, const int32_t* gm, const int32_t* gb, uint32_t 
                 uint32_t chunk, uint32_t maxch, const float* ws, float* out, cudaStream_t st) {
   arg_check(groups >= 1 && groups <= 1024, "colsum.groups: must be in [1, 1024]");
   if (!num_b || !N) return;
-  launch_pdl(seg_colsum_kernel, dim3(num_b, (unsigned)ceil_div((uint64_t)N, (uint64_t)RT)), RT, 0, st,
+  launch_pdl(seg_colsum_kernel, dim3(num_b, (unsigned)ceil_div((uint64_t)N, (uint64_t)32)), RT, 0, st,
              groups, gm, gb, N, chunk, maxch, ws, out);
   MOE_LAUNCH_CHECK("seg_colsum_kernel");
   count_launch();

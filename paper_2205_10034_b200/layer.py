@@ -10,7 +10,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 from dataclasses import dataclass
-from typing import Dict, Optional
+from typing import Dict, List, Optional, Tuple
 
 import torch
 
@@ -272,14 +272,18 @@ class MoELayer:
     def set_profiling(self, on: bool) -> None:
         call("moe_layer_set_profiling", self._h, 1 if on else 0)
 
-    def phase_times(self) -> Dict[str, float]:
+    def phase_list(self) -> List[Tuple[str, float]]:
+        """(phase, ms) of the last forward/backward in launch order (profiling on)."""
         names = (C.c_char_p * 64)()
         ms = (C.c_float * 64)()
         n = C.c_uint32(0)
         call("moe_layer_phase_times", self._h, names, ms, 64, C.byref(n))
+        return [(names[i].decode(), float(ms[i])) for i in range(n.value)]
+
+    def phase_times(self) -> Dict[str, float]:
         out: Dict[str, float] = {}
-        for i in range(n.value):
-            out[names[i].decode()] = out.get(names[i].decode(), 0.0) + ms[i]
+        for name, ms in self.phase_list():
+            out[name] = out.get(name, 0.0) + ms
         return out
 
     def close(self):

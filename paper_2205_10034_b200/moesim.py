@@ -409,3 +409,63 @@ def build_schedule(num_layers: int, ring_slots: int) -> RingSchedule:
     res = [RingOp(int(k), int(l), int(s), None if w < 0 else int(w))
            for k, l, s, w in ops[: n.value]]
     return RingSchedule(res, slots.value, bool(clamped.value))
+
+
+# ------------------------------------------------------------ timelines ----
+@dataclass
+class TaskRecord:
+    """sim_engine.hpp:28-34 TaskRecord (times in ns)."""
+    id: int
+    label: str
+    stream: str
+    start: int
+    end: int
+
+
+def timeline_to_trace_json(tasks: Sequence[TaskRecord]) -> dict:
+    """trace_export.cpp:28-50 timeline_to_trace_json: one thread_name metadata
+    event per stream (streams in name order, tid = that order), then one
+    complete ("X") event per task in submission order, times in us."""
+    tids = {name: i for i, name in enumerate(sorted({t.stream for t in tasks}))}
+    events = [{"args": {"name": n}, "name": "thread_name", "ph": "M", "pid": 1, "tid": i}
+              for n, i in tids.items()]
+    for t in tasks:
+        events.append({"args": {"task_id": t.id}, "dur": (t.end - t.start) / 1000.0,
+                       "name": t.label, "ph": "X", "pid": 1, "tid": tids[t.stream],
+                       "ts": t.start / 1000.0})
+    return {"displayTimeUnit": "ns", "traceEvents": events}
+
+
+def export_trace(tasks: Sequence[TaskRecord], path: str) -> None:
+    """trace_export.cpp:52-57 export_trace (ConfigError on an unwritable path)."""
+    import json
+    try:
+        with open(path, "w") as f:
+            f.write(json.dumps(timeline_to_trace_json(tasks), indent=2, sort_keys=True) + "\n")
+    except OSError as e:
+        raise ConfigError(f"trace: cannot open '{path}' for writing") from e
+
+
+def layer_step_timeline(phases: Sequence[tuple], stream: str = "compute",
+                        t0_ns: int = 0) -> List[TaskRecord]:
+    """Timeline of one layer step from its per-phase CUDA-event durations
+    (MoELayer.phase_times(), in launch order; the phases of one call are back
+    to back on the launch stream, so start = running sum).  phases: (label, ms)."""
+    out, t = [], int(t0_ns)
+    for i, (label, ms) in enumerate(phases):
+        d = int(round(ms * 1e6))
+        out.append(TaskRecord(i, label, stream, t, t + d))
+        t += d
+    return out
+
+
+def ring_timeline(tl: dict) -> List[TaskRecord]:
+    """Timeline of a ring-of-sections pass (RingOfSections.run's event times,
+    ms from the first load): section loads on "h2d", layer computes on
+    "compute" -- the streams of ring_offload.cpp:52-106."""
+    out = []
+    for i, (s, e) in enumerate(zip(tl["load_start"], tl["load_end"])):
+        out.append(TaskRecord(len(out), f"load[{i}]", "h2d", int(s * 1e6), int(e * 1e6)))
+    for i, (s, e) in enumerate(zip(tl["compute_start"], tl["compute_end"])):
+        out.append(TaskRecord(len(out), f"compute[{i}]", "compute", int(s * 1e6), int(e * 1e6)))
+    return out
