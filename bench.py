@@ -41,8 +41,10 @@ CONFIGS = {
                desc="c3: E=32 top-2, gate bias calibrated so the top-1 choice follows "
                     "gen_trace's Zipf(s=1.2) expert distribution (workload.cpp:19-53), capacity "
                     "drops, d=1024, d_ff=4096, T=65536/GPU, bf16 fwd+bwd"),
-    "c4": dict(E=64, k=2, d=4096, dff=16384, T=16384, cf=1.25, dtype="bf16",
-               desc="c4: GPT-MoE block d=4096, d_ff=16384, E=64 top-2, T=16384/GPU, bf16 fwd+bwd"),
+    "c4": dict(E=64, k=2, d=4096, dff=16384, T=16384, cf=1.25, dtype="bf16", layers=2,
+               desc="c4: GPT-MoE block stack of 2 MoE layers d=4096, d_ff=16384, E=64 top-2, "
+                    "T=16384/GPU, bf16 fwd+bwd; the layers' replicated gate gradients reduced by "
+                    "fused gradient buckets (moe_grad_buckets) at N>1"),
 }
 
 
@@ -372,6 +374,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--tokens", type=int, default=0, help="override T (tokens per GPU)")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="override the MoE layers per step (block stack; c4 default 2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ring", action="store_true",
@@ -388,6 +392,9 @@ def main():
     cfg = dict(CONFIGS[args.config])
     if args.tokens:
         cfg["T"] = args.tokens
+    if args.layers:
+        cfg["layers"] = args.layers
+    L = int(cfg.get("layers", 1))
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
@@ -411,17 +418,22 @@ def main():
     E, k, d, dff, T, cf = cfg["E"], cfg["k"], cfg["d"], cfg["dff"], cfg["T"], cfg["cf"]
     mcfg = MoEConfig(E, k, d, dff, cf, T, dtype, gate_bias=bool(cfg.get("skew")),
                      exchange=args.exchange, placement=args.placement)
-    layer = MoELayer(mcfg, ep=ep, device=dev)
+    if L > 1:
+        from paper_2205_10034_b200.stack import MoEStack
+        model = MoEStack(mcfg, L, ep=ep, device=dev)
+        layer = model.layers[0]
+    else:
+        model = layer = MoELayer(mcfg, ep=ep, device=dev)
     gb = gate_bias_for(cfg)
     gb = None if gb is None else torch.tensor(gb, dtype=torch.float32, device=dev)
-    layer.init_params(1234, gate_bias=gb)
-    x = layer.make_input(1234)
-    dy = layer.make_input(1234, T_DY)
+    model.init_params(1234, gate_bias=gb)
+    x = model.make_input(1234)
+    dy = model.make_input(1234, T_DY)
     stream = torch.cuda.current_stream()
 
     def step():
-        layer.forward(x)
-        layer.backward(dy, d_aux=0.01)
+        model.forward(x)
+        model.backward(dy, d_aux=0.01)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -450,18 +462,18 @@ def main():
 
     # ---- separate profiled pass: per-phase CUDA events on the launch stream ----
     barrier()  # ranks leave the clock sampler at different times: re-align first
-    layer.set_profiling(True)
+    model.set_profiling(True)
     phase_tot = {}
     for _ in range(args.steps):
-        layer.forward(x)
-        fwd_ph = layer.phase_list()
+        model.forward(x)
+        fwd_ph = model.phase_list()
         for n, v in fwd_ph:
             phase_tot["fwd." + n] = phase_tot.get("fwd." + n, 0.0) + v
-        layer.backward(dy, d_aux=0.01)
-        bwd_ph = layer.phase_list()
+        model.backward(dy, d_aux=0.01)
+        bwd_ph = model.phase_list()
         for n, v in bwd_ph:
             phase_tot["bwd." + n] = phase_tot.get("bwd." + n, 0.0) + v
-    layer.set_profiling(False)
+    model.set_profiling(False)
     if args.timeline and rank == 0:
         # the last profiled step as the reference's trace-event JSON
         # (trace_export.cpp:28-58; TaskRecord per phase on the launch stream)
@@ -502,7 +514,7 @@ def main():
     if ws > 1:
         dist.all_reduce(kept_t)
     rows_local = float(kept_t.item()) / ws  # EP: on average each GPU computes T*k kept rows
-    flops_step = 6 * 2.0 * rows_local * d * dff
+    flops_step = L * 6 * 2.0 * rows_local * d * dff
     achieved_tf = flops_step / (gemm_ms / 1000.0) / 1e12 if gemm_ms > 0 else None
     prof_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     traffic = None
@@ -552,8 +564,8 @@ def main():
     for name in ("ffn1", "ffn2", "dgrad_ffn2", "dgrad_ffn1", "wgrad_w1", "wgrad_w2"):
         ms_k = sum(v for n, v in phase_tot.items() if n.split(".", 1)[-1] == name) / args.steps
         if ms_k > 0:
-            tf = 2.0 * rows_local * d * dff / (ms_k / 1000.0) / 1e12
-            gbs = gbytes[name] / (ms_k / 1000.0) / 1e9
+            tf = L * 2.0 * rows_local * d * dff / (ms_k / 1000.0) / 1e12
+            gbs = L * gbytes[name] / (ms_k / 1000.0) / 1e9
             per.append({"gemm": name, "ms": ms_k, "tflops": tf, "frac": tf / peak,
                         "hbm_GBps": gbs, "hbm_frac": gbs / pk["hbm_gbs"]})
     roof["per_gemm"] = per
@@ -583,8 +595,8 @@ def main():
     for name, nbytes in hbytes.items():
         ms_k = sum(v for n, v in phase_tot.items() if n.split(".", 1)[-1] == name) / args.steps
         if ms_k > 0:
-            gbs = nbytes / (ms_k / 1000.0) / 1e9
-            hbm.append({"kernel": name, "us": 1000.0 * ms_k, "bytes": nbytes, "GBps": gbs,
+            gbs = L * nbytes / (ms_k / 1000.0) / 1e9
+            hbm.append({"kernel": name, "us": 1000.0 * ms_k, "bytes": L * nbytes, "GBps": gbs,
                         "frac": gbs / pk["hbm_gbs"]})
     roof["hbm_kernels"] = hbm
 
@@ -595,12 +607,24 @@ def main():
         dyh = dy.cpu().pin_memory()
         yh = torch.empty_like(xh).pin_memory()
         dxh = torch.empty_like(xh).pin_memory()
-        layer.train_step_host(xh, dyh, yh, dxh, d_aux=0.01)
+        if L == 1:
+            def host_step():
+                layer.train_step_host(xh, dyh, yh, dxh, d_aux=0.01, deferred=True)
+        else:  # block stack: H2D, stack fwd + bwd, D2H on the stream
+            def host_step():
+                xd = xh.to(dev, non_blocking=True)
+                dyd = dyh.to(dev, non_blocking=True)
+                yh.copy_(model.forward(xd), non_blocking=True)
+                dxh.copy_(model.backward(dyd, d_aux=0.01), non_blocking=True)
+        host_step()
+        if L == 1:
+            layer.host_sync()
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            layer.train_step_host(xh, dyh, yh, dxh, d_aux=0.01, deferred=True)
-        layer.host_sync()  # the last step's y / dx have landed in host memory
+            host_step()
+        if L == 1:
+            layer.host_sync()  # the last step's y / dx have landed in host memory
         ev1.record(stream)
         barrier()
         e_ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
@@ -611,8 +635,10 @@ def main():
         e2e = {"value": ws * T * args.steps / (e_ms / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
                "ms_per_step": e_ms / args.steps,
-               "api": "moe_layer_train_step_host_async x K + moe_layer_host_sync "
-                      "(pinned x, dy -> y, dx; every step's copies inside the timed region)",
+               "api": ("moe_layer_train_step_host_async x K + moe_layer_host_sync "
+                       "(pinned x, dy -> y, dx; every step's copies inside the timed region)")
+                      if L == 1 else "MoEStack fwd/bwd with pinned x, dy -> y, dx copies "
+                                     "on the stream",
                "host_cpus_bound": numa_cpus}
 
     cpu = None
@@ -629,7 +655,7 @@ def main():
     ring = None
     if rank == 0 and ws == 1 and not args.no_ring and dtype == torch.bfloat16:
         ring = ring_leg(args, dev)
-    a2a_fusion = a2a_fusion_leg(ep, ws, rank, E, layer.capacity, d) if ws > 1 else None
+    a2a_fusion = a2a_fusion_leg(ep, ws, rank, E, model.capacity, d) if ws > 1 else None
 
     a2a_ms = sum(v for n, v in phase_tot.items() if ".a2a" in n) / args.steps
     nvlink = None
@@ -637,7 +663,7 @@ def main():
         # token rows that cross NVLink per exchange per GPU: kept rows owned by
         # other ranks (uniform routing: (P-1)/P of them), d * 2 bytes each
         row_bytes = d * (2 if dtype == torch.bfloat16 else 4)
-        xbytes = kept_local * row_bytes * (ws - 1) / ws
+        xbytes = L * kept_local * row_bytes * (ws - 1) / ws  # summed over the stack's layers
         ph = {n: v / args.steps for n, v in phase_tot.items()}
         if args.exchange == "p2p":
             ex = {"dispatch": ph.get("fwd.dispatch_p2p", 0) + ph.get("fwd.a2a_dispatch", 0),
@@ -675,7 +701,7 @@ def main():
         "data": "synthetic (SplitMix64-seeded x, dy and weights; rng.hpp substreams)",
         "config": {"workload": cfg["desc"], "tokens_per_gpu": T, "experts": E, "top_k": k,
                    "d_model": d, "d_ff": dff, "capacity_factor": cf,
-                   "capacity": layer.capacity, "experts_per_gpu": E // ws,
+                   "capacity": model.capacity, "experts_per_gpu": E // ws, "layers": L,
                    "parallelism": f"ep{ws}" if ws > 1 else "single",
                    "exchange": args.exchange if ws > 1 else None,
                    "placement": args.placement if ws > 1 else None,
@@ -696,7 +722,7 @@ def main():
     if rank == 0:
         emit(line)
     if ep is not None:
-        layer.close()
+        model.close()
         ep.close()
         dist.destroy_process_group()
 

@@ -245,6 +245,9 @@ typedef struct moe_layer_desc {
   void* nccl_comm;         /* ncclComm_t when ep_size > 1 (see moe_comm_*) */
   uint32_t exchange;       /* ep_size > 1: MOE_EXCHANGE_P2P (default) or MOE_EXCHANGE_NCCL */
   uint32_t placement;      /* ep_size > 1: MOE_PLACEMENT_CONTIGUOUS (default) or _ROUND_ROBIN */
+  uint32_t gate_grad_reduce; /* ep_size > 1: 0 = backward sums the replicated gate gradients
+                                dwg/dbg over the EP group (default); 1 = left to the caller,
+                                e.g. one fused moe_grad_buckets all-reduce for a layer stack */
 } moe_layer_desc_t;
 
 /* Expert placement over the ep_size ranks.  CONTIGUOUS: expert e lives on rank

@@ -163,6 +163,7 @@ class LayerDesc(C.Structure):
         ("nccl_comm", C.c_void_p),
         ("exchange", C.c_uint32),
         ("placement", C.c_uint32),
+        ("gate_grad_reduce", C.c_uint32),
     ]
 
 

@@ -69,6 +69,7 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   config_check(E % P == 0, "layer.ep_size: must divide num_experts");
   config_check(rank < P, "layer.ep_rank: must be < ep_size");
   config_check(P == 1 || d.nccl_comm != nullptr, "layer.nccl_comm: required when ep_size > 1");
+  config_check(d.gate_grad_reduce <= 1, "layer.gate_grad_reduce: must be 0 (layer) or 1 (caller)");
   config_check(d.placement == MOE_PLACEMENT_CONTIGUOUS || d.placement == MOE_PLACEMENT_ROUND_ROBIN,
                "layer.placement: must be MOE_PLACEMENT_CONTIGUOUS or MOE_PLACEMENT_ROUND_ROBIN");
   if (dt == MOE_DTYPE_BF16) {
@@ -443,7 +444,8 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   }
   // the replicated gate gradients are final here: push them to the peers now
   // so the closing all-reduce only sums (no wait on a late peer's push)
-  if (p2p)
+  const bool reduce_gate = desc.gate_grad_reduce == 0;
+  if (p2p && reduce_gate)
     p2p_allreduce_push(win, g.dwg, (uint64_t)E * dm, desc.has_gate_bias ? g.dbg : nullptr,
                        desc.has_gate_bias && g.dbg ? E : 0, ph, st);
   mark("gate_wgrad", st);
@@ -574,11 +576,11 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("gate_dgrad_gather_dx", st);
-  if (p2p) {
+  if (p2p && reduce_gate) {
     // replicated gate gradients: sum the pushed partials in rank order
     p2p_allreduce_finish(win, g.dwg, (uint64_t)E * dm, desc.has_gate_bias ? g.dbg : nullptr,
                          desc.has_gate_bias && g.dbg ? E : 0, ph, st);
-  } else if (P > 1) {
+  } else if (P > 1 && reduce_gate) {
     MOE_NCCL(ncclGroupStart());
     MOE_NCCL(ncclAllReduce(g.dwg, g.dwg, (uint64_t)E * dm, ncclFloat32, ncclSum, (ncclComm_t)comm, st));
     if (desc.has_gate_bias && g.dbg)

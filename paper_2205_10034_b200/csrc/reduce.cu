@@ -7,50 +7,71 @@
 // gradients are bitwise reproducible run to run — the reference's simulator
 // is deterministic by construction (acceptance_main.cpp:442-486).
 //
-// Both kernels are HBM/L2-bound streaming reductions: a warp reads 32
-// adjacent outputs of one partial (a coalesced 128-byte line), eight warps
-// split the partials and are combined in a fixed order.
+// Both kernels are HBM/L2-bound streaming reductions: a warp reads 128
+// adjacent outputs of one partial (512 contiguous bytes, float4 per lane),
+// eight warps split the partials and are combined in a fixed order.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace moe {
 namespace {
 
-// Block = 32 output columns x PW part-groups: lane = column, warp w sums the
-// partials p = w, w + PW, ... (all its loads independent), then warp 0 adds
-// the PW group sums in order -- a fixed summation order, bitwise reproducible.
+// Block = 32 lanes x PW part-groups: lane = 4 adjacent outputs (one float4,
+// a warp covers 512 contiguous bytes of a partial row), warp w sums the
+// partials p = w, w + PW, ... with every load of its loop in flight, then
+// warp 0 adds the PW group sums in order -- a fixed summation order.
 constexpr int PW = 8;
 constexpr int RT = 32 * PW;
 
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
 // out[r*cols + c] (transpose: out[c*rows + r]) = sum_{p < nparts} part[p*pstride + r*ldp + c]
+// VEC: cols % 4 == 0, ldp % 4 == 0, pstride % 4 == 0 (float4 loads)
+template <bool VEC>
 __global__ void __launch_bounds__(RT) sum_parts_kernel(const float* __restrict__ part,
                                                        uint32_t nparts, uint64_t pstride,
                                                        uint64_t rows, uint64_t cols, uint64_t ldp,
                                                        int transpose, float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float red[PW][32];
+  constexpr int V = VEC ? 4 : 1;
+  __shared__ float4 red[PW][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint64_t i = (uint64_t)blockIdx.x * 32 + lane;
+  const uint64_t i = ((uint64_t)blockIdx.x * 32 + lane) * V;  // first of this lane's outputs
   const bool ok = i < rows * cols;
   const uint64_t r = ok ? i / cols : 0, c = ok ? i % cols : 0;
   const float* p = part + r * ldp + c;
-  float s = 0.f;
-  if (ok)
-    for (uint32_t q = w; q < nparts; q += PW) s += __ldcg(p + (uint64_t)q * pstride);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ok) {
+    auto ld = [&](uint32_t q) -> float4 {
+      if (VEC) return __ldcg(reinterpret_cast<const float4*>(p + (uint64_t)q * pstride));
+      return make_float4(__ldcg(p + (uint64_t)q * pstride), 0.f, 0.f, 0.f);
+    };
+    uint32_t q = w;
+    for (; q + 3 * PW < nparts; q += 4 * PW) {  // four loads in flight, summed in order
+      const float4 a0 = ld(q), a1 = ld(q + PW), a2 = ld(q + 2 * PW), a3 = ld(q + 3 * PW);
+      s = add4(add4(add4(add4(s, a0), a1), a2), a3);
+    }
+    for (; q < nparts; q += PW) s = add4(s, ld(q));
+  }
   red[w][lane] = s;
   __syncthreads();
   if (w == 0 && ok) {
-    float t = red[0][lane];
+    float4 t = red[0][lane];
 #pragma unroll
-    for (int k = 1; k < PW; ++k) t += red[k][lane];
-    out[transpose ? c * rows + r : i] = t;
+    for (int k = 1; k < PW; ++k) t = add4(t, red[k][lane]);
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[transpose ? (c + v) * rows + r : i + v] = tv[v];
   }
 }
 
 // out[b][n] = sum over groups g (ascending) with gb[g] == b of
 //             sum over chunks ch < ceil(gm[g] / chunk) of ws[(g*maxch + ch)*N + n]
-// (chunks split over the PW warps like sum_parts)
+// (chunks split over the PW warps like sum_parts; VEC: N % 4 == 0)
+template <bool VEC>
 __global__ void __launch_bounds__(RT) seg_colsum_kernel(uint32_t groups, const int32_t* __restrict__ gm,
                                                         const int32_t* __restrict__ gb, uint32_t N,
                                                         uint32_t chunk, uint32_t maxch,
@@ -58,32 +79,37 @@ __global__ void __launch_bounds__(RT) seg_colsum_kernel(uint32_t groups, const i
                                                         float* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
-  __shared__ int s_nch[1024];
-  __shared__ int s_b[1024];
-  __shared__ float red[PW][32];
+  constexpr int V = VEC ? 4 : 1;
+  __shared__ float4 red[PW][32];
   const int b = blockIdx.x;
-  for (uint32_t g = threadIdx.x; g < groups; g += RT) {
-    s_b[g] = gb[g];
-    s_nch[g] = min((int)maxch, (gm[g] + (int)chunk - 1) / (int)chunk);
-  }
-  __syncthreads();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t n = blockIdx.y * 32 + lane;
-  float s = 0.f;
+  const uint32_t n = (blockIdx.y * 32 + lane) * V;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (n < N) {
     for (uint32_t g = 0; g < groups; ++g) {
-      if (s_b[g] != b) continue;
+      if (__ldg(gb + g) != b) continue;
+      const int nch = min((int)maxch, (__ldg(gm + g) + (int)chunk - 1) / (int)chunk);
       const float* p = ws + (uint64_t)g * maxch * N + n;
-      for (int ch = w; ch < s_nch[g]; ch += PW) s += __ldcg(p + (uint64_t)ch * N);
+      auto ld = [&](int ch) -> float4 {
+        if (VEC) return __ldcg(reinterpret_cast<const float4*>(p + (uint64_t)ch * N));
+        return make_float4(__ldcg(p + (uint64_t)ch * N), 0.f, 0.f, 0.f);
+      };
+      int ch = w;
+      for (; ch + 3 * PW < nch; ch += 4 * PW) {  // four loads in flight, summed in order
+        const float4 a0 = ld(ch), a1 = ld(ch + PW), a2 = ld(ch + 2 * PW), a3 = ld(ch + 3 * PW);
+        s = add4(add4(add4(add4(s, a0), a1), a2), a3);
+      }
+      for (; ch < nch; ch += PW) s = add4(s, ld(ch));
     }
   }
   red[w][lane] = s;
   __syncthreads();
   if (w == 0 && n < N) {
-    float t = red[0][lane];
+    float4 t = red[0][lane];
 #pragma unroll
-    for (int k = 1; k < PW; ++k) t += red[k][lane];
-    out[(uint64_t)b * N + n] = t;
+    for (int k = 1; k < PW; ++k) t = add4(t, red[k][lane]);
+    if (VEC) *reinterpret_cast<float4*>(out + (uint64_t)b * N + n) = t;
+    else out[(uint64_t)b * N + n] = t.x;
   }
 }
 
@@ -93,8 +119,14 @@ void sum_parts(const float* part, uint32_t nparts, uint64_t part_stride, uint64_
                uint64_t cols, uint64_t ldp, bool transpose, float* out, cudaStream_t st) {
   const uint64_t n = rows * cols;
   if (!n) return;
-  launch_pdl(sum_parts_kernel, (unsigned)ceil_div(n, (uint64_t)32), RT, 0, st, part, nparts,
-             part_stride, rows, cols, ldp, transpose ? 1 : 0, out);
+  const bool vec = cols % 4 == 0 && ldp % 4 == 0 && part_stride % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(part) & 15) == 0;
+  if (vec)
+    launch_pdl(sum_parts_kernel<true>, (unsigned)ceil_div(n, (uint64_t)128), RT, 0, st, part,
+               nparts, part_stride, rows, cols, ldp, transpose ? 1 : 0, out);
+  else
+    launch_pdl(sum_parts_kernel<false>, (unsigned)ceil_div(n, (uint64_t)32), RT, 0, st, part,
+               nparts, part_stride, rows, cols, ldp, transpose ? 1 : 0, out);
   MOE_LAUNCH_CHECK("sum_parts_kernel");
   count_launch();
 }
@@ -103,8 +135,14 @@ void seg_colsum(uint32_t groups, const int32_t* gm, const int32_t* gb, uint32_t 
                 uint32_t chunk, uint32_t maxch, const float* ws, float* out, cudaStream_t st) {
   arg_check(groups >= 1 && groups <= 1024, "colsum.groups: must be in [1, 1024]");
   if (!num_b || !N) return;
-  launch_pdl(seg_colsum_kernel, dim3(num_b, (unsigned)ceil_div((uint64_t)N, (uint64_t)32)), RT, 0, st,
-             groups, gm, gb, N, chunk, maxch, ws, out);
+  const bool vec = N % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (vec)
+    launch_pdl(seg_colsum_kernel<true>, dim3(num_b, (unsigned)ceil_div((uint64_t)N, (uint64_t)128)),
+               RT, 0, st, groups, gm, gb, N, chunk, maxch, ws, out);
+  else
+    launch_pdl(seg_colsum_kernel<false>, dim3(num_b, (unsigned)ceil_div((uint64_t)N, (uint64_t)32)),
+               RT, 0, st, groups, gm, gb, N, chunk, maxch, ws, out);
   MOE_LAUNCH_CHECK("seg_colsum_kernel");
   count_launch();
 }

@@ -71,6 +71,7 @@ class MoEConfig:
     gate_bias: bool = False
     exchange: str = "p2p"  # EP token exchange: "p2p" (NVLink peer stores) or "nccl"
     placement: str = "contiguous"  # expert placement over ranks: "contiguous" or "round_robin"
+    gate_grad_reduce: str = "layer"  # EP gate-gradient sum: "layer" (in backward) or "caller"
 
 
 class EPGroup:
@@ -133,6 +134,9 @@ class MoELayer:
         if cfg.placement not in ("contiguous", "round_robin"):
             raise _lib.ConfigError("layer.placement: must be 'contiguous' or 'round_robin'")
         desc.placement = 0 if cfg.placement == "contiguous" else 1
+        if cfg.gate_grad_reduce not in ("layer", "caller"):
+            raise _lib.ConfigError("layer.gate_grad_reduce: must be 'layer' or 'caller'")
+        desc.gate_grad_reduce = 0 if cfg.gate_grad_reduce == "layer" else 1
         h = C.c_void_p()
         if self.device.type == "cuda":
             with torch.cuda.device(self.device):

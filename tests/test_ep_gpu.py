@@ -98,6 +98,43 @@ def _worker(rank, world, port, case, q):
             gb.close()
             q.put((rank, "ok"))
             return
+        if isinstance(case, tuple) and case[0] == "stack":
+            # config c4 as a block stack: gate gradients reduced by ONE fused
+            # bucket all-reduce per step == each layer reducing its own
+            from paper_2205_10034_b200.stack import MoEStack
+            _, E, k, d, dff, T, L, exch = case
+            cfg = MoEConfig(E, k, d, dff, 1.25, T, torch.bfloat16, exchange=exch, gate_bias=True)
+            st = MoEStack(cfg, L, ep=ep)
+            st.init_params(5)
+            ref_layers = [MoELayer(cfg, ep=ep) for _ in range(L)]
+            for i, rl in enumerate(ref_layers):
+                rl.init_params((5 ^ (0x9E3779B97F4A7C15 * (i + 1))) & ((1 << 64) - 1))
+            x = st.make_input(5)
+            dy = st.make_input(5, T_DY)
+            for _ in range(2):
+                y = st.forward(x)
+                dx = st.backward(dy, d_aux=0.02)
+            h = x
+            for rl in ref_layers:
+                h = rl.forward(h)
+            g = dy
+            for rl in reversed(ref_layers):
+                g = rl.backward(g, d_aux=0.02)
+            torch.cuda.synchronize()
+            assert torch.equal(y, h) and torch.equal(dx, g), "stack output / dx differ"
+            for sl, rl in zip(st.layers, ref_layers):
+                for n in ("dwg", "dbg"):
+                    err = (sl.grads[n] - rl.grads[n]).abs().max() / rl.grads[n].abs().max()
+                    assert err < 1e-5, (n, err.item())
+                for n in ("dw1", "dw2"):
+                    assert torch.equal(sl.grads[n], rl.grads[n]), n
+            st.close()
+            for rl in ref_layers:
+                rl.close()
+            ep.close()
+            dist.destroy_process_group()
+            q.put((rank, "ok"))
+            return
         E, k, d, dff, T, dt, exch = case[:7]
         placement = case[7] if len(case) > 7 else "contiguous"
         cfg = MoEConfig(E, k, d, dff, 1.25, T, dt, exchange=exch, placement=placement)
@@ -183,6 +220,14 @@ def test_gradient_buckets_allreduce():
 ])
 def test_ep_layer_matches_single_gpu(case):
     _run(case, world=min(torch.cuda.device_count(), 2))
+
+
+@pytest.mark.parametrize("exch", ["p2p", "nccl"])
+def test_ep_block_stack_fused_gate_gradients(exch):
+    """c4 block stack (3 layers): gate gradients of all layers reduced by fused
+    moe_grad_buckets all-reduces (the layers' own reduction off) match the
+    per-layer reduction; activations, dx and expert gradients bit-identical."""
+    _run(("stack", 16, 2, 256, 512, 1024, 3, exch), world=min(torch.cuda.device_count(), 2))
 
 
 @pytest.mark.parametrize("case", [

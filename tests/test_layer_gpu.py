@@ -352,3 +352,27 @@ def test_gradients_bitwise_deterministic(dtype, E, k, d, dff, T):
     for r in runs[1:]:
         for n, t in runs[0].items():
             assert torch.equal(t, r[n]), n
+
+
+def test_block_stack_single_gpu_equals_chained_layers():
+    """MoEStack (config c4's block stack) on one GPU == the layers chained by
+    hand, forward and backward, bit for bit."""
+    from paper_2205_10034_b200.stack import MoEStack
+    cfg = MoEConfig(16, 2, 256, 512, 1.25, 1024, torch.bfloat16)
+    st = MoEStack(cfg, 2)
+    st.init_params(3)
+    x = st.make_input(3)
+    dy = st.make_input(3, T_DY)
+    y = st.forward(x)
+    dx = st.backward(dy, d_aux=0.01)
+    a = MoELayer(cfg)
+    b = MoELayer(cfg)
+    a.init_params((3 ^ 0x9E3779B97F4A7C15) & ((1 << 64) - 1))
+    b.init_params((3 ^ (2 * 0x9E3779B97F4A7C15)) & ((1 << 64) - 1))
+    y2 = b.forward(a.forward(x))
+    dx2 = a.backward(b.backward(dy, d_aux=0.01), d_aux=0.01)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2) and torch.equal(dx, dx2)
+    for n in ("dwg", "dw1", "dw2", "db1", "db2"):
+        assert torch.equal(st.layers[0].grads[n], a.grads[n]), n
+        assert torch.equal(st.layers[1].grads[n], b.grads[n]), n
