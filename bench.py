@@ -529,7 +529,14 @@ def main():
         kname, bound = ("tc_gemm_kernel (6 expert GEMMs/step: ffn1, ffn2, 2x dgrad, 2x wgrad)",
                         "tensor")
         psrc = pk["source"] + (", burst (timed region at max SM clock)" if burst else ", sustained")
-    else:  # c1: fp32 SIMT GEMMs (TF32 would break the 1e-5 tolerance)
+    elif ws == 1 and d % 128 == 0 and dff % 128 == 0 and os.environ.get("MOE_F32_GEMM") != "simt":
+        # c1: fp32 expert GEMMs as split-bf16 tcgen05 GEMMs (f32split.cu): six
+        # bf16 plane products per fp32 product, so the fp32 ceiling is 1/6 of bf16
+        peak = (pk["bf16_tflops"] if burst else pk["bf16_tflops_sustained"]) / 6.0
+        kname, bound = ("tc_gemm_kernel split-fp32 (6 expert GEMMs/step as 6 bf16 plane products, "
+                        "K chunks of 512 summed in fp32; incl. split / finish kernels)", "tensor")
+        psrc = pk["source"] + (", burst" if burst else ", sustained") + " bf16 / 6"
+    else:  # fp32 SIMT GEMMs
         props = torch.cuda.get_device_properties(dev)
         peak = props.multi_processor_count * 128 * 2 * pk.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         kname, bound = "simt_gemm_kernel (6 expert GEMMs/step, fp32 FFMA)", "fp32"

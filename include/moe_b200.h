@@ -223,9 +223,21 @@ typedef struct moe_gemm_problem {
   uint32_t gather_k;
   float* colsum_ws;       /* DGELU with colsum: partials [groups][ceil(colsum_max_m/32)][N] */
   uint64_t colsum_max_m;  /* DGELU with colsum: upper bound of m[g] over the groups      */
+  /* split-fp32 products on the bf16 tensor cores (fp32 STORE only): with
+   * split_terms = 6, A and B each hold three stacked bf16 planes of an fp32
+   * tensor (x = p0 + p1 + p2, moe_split_f32_bf16x3), plane j at row offset j x
+   * (a_rows | b_rows, the single-plane row counts), and C = the sum of the six
+   * leading plane products (error ~2^-22 relative per product). */
+  uint32_t split_terms;   /* 0 or 1: plain; 6: split-fp32                                */
+  uint32_t k_begin;       /* RAGGED_M: K sub-range [k_begin, k_begin + k_len) (multiples */
+  uint32_t k_len;         /*   of 64; k_len 0 = to K) -- bounds accumulation chains      */
 } moe_gemm_problem_t;
 
 moe_status_t moe_grouped_gemm(const moe_gemm_problem_t* problem, void* stream);
+
+/* fp32 -> three stacked bf16 planes (n elements each) with in = p0 + p1 + p2
+ * exactly (the split_terms = 6 operand format); n % 4 == 0, in 16-byte aligned. */
+moe_status_t moe_split_f32_bf16x3(const float* in, uint64_t n, void* out, void* stream);
 
 /* ======================================================================
  * 3. the MoE layer (K1..K6 + EP exchange), forward and backward

@@ -117,6 +117,9 @@ class GemmProblem(C.Structure):
         ("gather_k", C.c_uint32),
         ("colsum_ws", C.c_void_p),
         ("colsum_max_m", C.c_uint64),
+        ("split_terms", C.c_uint32),
+        ("k_begin", C.c_uint32),
+        ("k_len", C.c_uint32),
     ]
 
 
@@ -234,6 +237,7 @@ SIGNATURES = {
     "moe_layer_train_step_host_async": (_I, [_VP, C.POINTER(LayerParams), _VP, _VP, _F, _VP,
                                              _VP, C.POINTER(LayerGrads), _VP]),
     "moe_layer_host_sync": (_I, [_VP, _VP]),
+    "moe_split_f32_bf16x3": (_I, [_VP, _U64, _VP, _VP]),
     "moe_layer_set_profiling": (_I, [_VP, _I]),
     "moe_layer_set_peer_timeout": (_I, [_VP, C.c_double]),
     "moe_layer_comm_status": (_I, [_VP, C.POINTER(C.c_int32)]),

@@ -405,6 +405,13 @@ moe_status_t moe_grouped_gemm(const moe_gemm_problem_t* problem, void* stream) {
   });
 }
 
+moe_status_t moe_split_f32_bf16x3(const float* in, uint64_t n, void* out, void* stream) {
+  return guard([&] {
+    moe::arg_check(n == 0 || (in != nullptr && out != nullptr), "split.in/out: must be non-null");
+    moe::split_f32_bf16x3(in, n, out, S(stream));
+  });
+}
+
 // ------------------------------------------------------------- layer -----
 moe_status_t moe_layer_create(const moe_layer_desc_t* desc, moe_layer_t* out) {
   return guard([&] {

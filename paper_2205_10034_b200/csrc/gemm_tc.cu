@@ -106,7 +106,20 @@ struct Args {
   int transpose_c;
   int num_b;
   int c_direct;  // C rows not 16-byte aligned (e.g. N = E = 2): no TMA stores, scalar stores
+  // split-fp32 mode (terms == 6): A and B are three stacked bf16 planes each
+  // (x = p0 + p1 + p2), a_plane / b_plane rows apart; the K loop runs the six
+  // leading plane products, the main one (p0 q0) last; K range [k_begin,
+  // k_begin + k_len) (RAGGED_M) so the caller can bound the accumulation chains
+  int terms;
+  long long a_plane, b_plane;
+  int k_begin, k_len;
 };
+
+// plane pairs of the split-fp32 products, smallest first: the tensor core's
+// fp32 accumulation truncates (tc_accum_probe.py: -168 ulp mean at K = 4096),
+// so the large p0 q0 chain goes last onto an accumulator still small
+__constant__ int kSplitA[6] = {2, 1, 0, 1, 0, 0};
+__constant__ int kSplitB[6] = {0, 1, 2, 0, 1, 0};
 
 // Per-peer destinations of the remote-store epilogue (RemoteRows on device).
 struct RemoteOut {
@@ -312,10 +325,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   };
   auto num_kblocks = [&](int g) -> int {
-    if (KIND == 0) return args.K / BK;
+    if (KIND == 0) return (args.k_len / BK) * args.terms;
     int n = 0;
     for (int q = tab[g]; q < tab[g + 1]; ++q) n += (args.gm[q] + BK - 1) / BK;
-    return n;
+    return n * args.terms;
   };
 
   // Last block of a ragged group with <= 128 rows left: run it as an M = 128
@@ -354,38 +367,50 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int arow = args.ga[g] + mb * TM + (int)crank * (is_tail(g, mb) ? 64 : BM);
           const int brow = args.gb[g] * (B_MN ? args.K : args.N);
           const int bcol = nb * BN + (int)crank * BH;
-          const int nkb = args.K / BK;
-          for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int nk = args.k_len / BK, kb0 = args.k_begin / BK;
+          const int nkb = nk * args.terms;
+          for (int i = 0; i < nkb; ++i, ++it) {
+            const int t = args.terms == 1 ? 0 : i / nk;
+            const int kb = kb0 + (args.terms == 1 ? i : i % nk);
+            const int pa = args.terms == 1 ? 0 : (int)(kSplitA[t] * args.a_plane);
+            const int pb = args.terms == 1 ? 0 : (int)(kSplitB[t] * args.b_plane);
             const int s = it % C_::STAGES;
             mbar_wait(&empty[s], ((it / C_::STAGES) & 1) ^ 1);
             uint8_t* sA = smem + s * C_::STAGE_BYTES;
             uint8_t* sB = sA + C_::A_BYTES;
             arm(s);
-            load(sA, &tmA, s, kb * BK, arow);  // A K-major box {64,128}
+            load(sA, &tmA, s, kb * BK, arow + pa);  // A K-major box {64,128}
             if (!B_MN) {
-              load(sB, &tmB, s, kb * BK, brow + bcol);
+              load(sB, &tmB, s, kb * BK, brow + bcol + pb);
             } else {
 #pragma unroll
-              for (int j = 0; j < BH / 64; ++j) load(sB + j * 8192, &tmB, s, bcol + j * 64, brow + kb * BK);
+              for (int j = 0; j < BH / 64; ++j)
+                load(sB + j * 8192, &tmB, s, bcol + j * 64, brow + pb + kb * BK);
             }
           }
         } else {
           const int acol = mb * TM + (int)crank * BM;
           const int bcol = nb * BN + (int)crank * BH;
-          for (int q = tab[g]; q < tab[g + 1]; ++q) {
-            const int rows = args.gm[q];
-            const int r0 = args.ga[q];
-            for (int kb = 0; kb * BK < rows; ++kb, ++it) {
-              const int s = it % C_::STAGES;
-              mbar_wait(&empty[s], ((it / C_::STAGES) & 1) ^ 1);
-              uint8_t* sA = smem + s * C_::STAGE_BYTES;
-              uint8_t* sB = sA + C_::A_BYTES;
-              arm(s);
-              const int row = r0 + kb * BK;
+          for (int t = 0; t < args.terms; ++t) {
+            const int pa = args.terms == 1 ? 0 : (int)(kSplitA[t] * args.a_plane);
+            const int pb = args.terms == 1 ? 0 : (int)(kSplitB[t] * args.b_plane);
+            for (int q = tab[g]; q < tab[g + 1]; ++q) {
+              const int rows = args.gm[q];
+              const int r0 = args.ga[q];
+              for (int kb = 0; kb * BK < rows; ++kb, ++it) {
+                const int s = it % C_::STAGES;
+                mbar_wait(&empty[s], ((it / C_::STAGES) & 1) ^ 1);
+                uint8_t* sA = smem + s * C_::STAGE_BYTES;
+                uint8_t* sB = sA + C_::A_BYTES;
+                arm(s);
+                const int row = r0 + kb * BK;
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) load(sA + j * 8192, &tmA, s, acol + j * 64, row);
+                for (int j = 0; j < BM / 64; ++j)
+                  load(sA + j * 8192, &tmA, s, acol + j * 64, row + pa);
 #pragma unroll
-              for (int j = 0; j < BH / 64; ++j) load(sB + j * 8192, &tmB, s, bcol + j * 64, row);
+                for (int j = 0; j < BH / 64; ++j)
+                  load(sB + j * 8192, &tmB, s, bcol + j * 64, row + pb);
+              }
             }
           }
         }
@@ -845,23 +870,32 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
     configured.fetch_or(bit, std::memory_order_acq_rel);
   }
   CUtensorMap ta, tb, tcm, tc2, tax;
+  const bool split = p.split_terms == 6;
+  // split-fp32: the maps span the three stacked planes
+  const uint64_t np = split ? 3 : 1;
+  uint64_t a_plane = 0, b_plane = 0;
   if (KIND == 0) {
     const uint64_t lda = p.lda ? p.lda : p.K;
-    ta = make_map(p.A, p.K, p.a_rows, lda, 64, BM);
+    a_plane = p.a_rows;
+    ta = make_map(p.A, p.K, np * p.a_rows, lda, 64, BM);
     if (!B_MN) {
       const uint64_t ldb = p.ldb ? p.ldb : p.K;
       const uint64_t rows = p.b_rows ? p.b_rows : (uint64_t)p.num_b * p.N;
-      tb = make_map(p.B, p.K, rows, ldb, 64, BH);
+      b_plane = rows;
+      tb = make_map(p.B, p.K, np * rows, ldb, 64, BH);
     } else {
       const uint64_t ldb = p.ldb ? p.ldb : p.N;
       const uint64_t rows = p.b_rows ? p.b_rows : (uint64_t)p.num_b * p.K;
-      tb = make_map(p.B, p.N, rows, ldb, 64, 64);
+      b_plane = rows;
+      tb = make_map(p.B, p.N, np * rows, ldb, 64, 64);
     }
   } else {
     const uint64_t lda = p.lda ? p.lda : p.M;
     const uint64_t ldb = p.ldb ? p.ldb : p.N;
-    ta = make_map(p.A, p.M, p.a_rows, lda, 64, 64);
-    tb = make_map(p.B, p.N, p.b_rows ? p.b_rows : p.a_rows, ldb, 64, 64);
+    a_plane = p.a_rows;
+    b_plane = p.b_rows ? p.b_rows : p.a_rows;
+    ta = make_map(p.A, p.M, np * p.a_rows, lda, 64, 64);
+    tb = make_map(p.B, p.N, np * b_plane, ldb, 64, 64);
   }
   const uint64_t c_rows = p.c_rows ? p.c_rows : (KIND == 0 ? p.a_rows : (uint64_t)p.num_b * p.M);
   tcm = tc2 = tax = ta;
@@ -897,6 +931,11 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   a.transpose_c = p.transpose_c;
   a.num_b = (int)p.num_b;
   a.c_direct = c_direct ? 1 : 0;
+  a.terms = split ? 6 : 1;
+  a.a_plane = (long long)a_plane;
+  a.b_plane = (long long)b_plane;
+  a.k_begin = (int)p.k_begin;
+  a.k_len = (int)(p.k_len ? p.k_len : p.K - p.k_begin);
   RemoteOut ro;  // remote descriptor (copied into the launch parameters)
   std::memset(&ro, 0, sizeof(ro));
   if (REMOTE) {
@@ -958,6 +997,12 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st, const RemoteR
   }
   arg_check(p.groups >= 1 && p.groups <= MAX_GROUPS, "gemm.groups: must be in [1, 1024]");
   arg_check(p.dtype_ab == MOE_DTYPE_BF16, "gemm.dtype_ab: tcgen05 path needs bf16");
+  arg_check(p.split_terms == 0 || p.split_terms == 1 ||
+                (p.split_terms == 6 && p.dtype_c == MOE_DTYPE_F32 && p.epilogue == MOE_EPI_STORE),
+            "gemm.split_terms: 0/1, or 6 (three bf16 planes per operand, fp32 STORE)");
+  arg_check(p.kind == MOE_GEMM_RAGGED_K ||
+                (p.k_begin % BK == 0 && p.k_len % BK == 0 && p.k_begin + p.k_len <= p.K),
+            "gemm.k_begin/k_len: multiples of 64 inside [0, K]");
   const bool f32 = p.dtype_c == MOE_DTYPE_F32;
   if (p.kind == MOE_GEMM_RAGGED_M) {
     arg_check(p.K % BK == 0, "gemm.K: must be a multiple of 64");

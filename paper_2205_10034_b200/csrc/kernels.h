@@ -130,6 +130,19 @@ inline uint64_t gemm_colsum_ws_floats(uint32_t groups, uint32_t N, uint64_t max_
   return (uint64_t)groups * ((max_m + 31) / 32) * N;
 }
 
+// fp32 GEMMs on the bf16 tensor cores (f32split.cu): x = p0 + p1 + p2 bf16
+// planes (out = 3 stacked planes of n), and the fused K-chunk sum + epilogue
+// (mode 0: + bias; 1: GeLU / GeLU' of (sum + bias) into out / out2; 2: sum x
+// aux) over the rows of each group, pad rows [m, stride) zeroed.
+void split_f32_bf16x3(const float* in, uint64_t n, void* out, cudaStream_t st);
+void split_finish(int mode, const float* part, int nparts, uint64_t part_stride, uint32_t groups,
+                  const int32_t* gm, const int32_t* ga, const int32_t* gb, uint32_t stride,
+                  uint32_t N, const float* bias, const float* aux, float* out, float* out2,
+                  cudaStream_t st);
+// row chunk c of every group: cm = clamp(m - c*chunk, 0, chunk), ca = a_row + c*chunk
+void chunk_groups(uint32_t groups, const int32_t* gm, const int32_t* ga, int chunk, int c,
+                  int32_t* cm, int32_t* ca, cudaStream_t st);
+
 // Round-robin placement relabel (include/moe_b200.h): pexpert = pi(expert),
 // pkept[pi(e)] = kept[e], pi(e) = (e % P) * (E / P) + e / P.
 void relabel_experts(uint64_t T, uint32_t k, uint32_t E, uint32_t P, const int32_t* expert,

@@ -84,7 +84,14 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   comm = d.nccl_comm;
   const double c = (double)k * d.capacity_factor * (double)T / (double)E;
   C = (uint64_t)std::ceil(c);
-  pad = dt == MOE_DTYPE_BF16 ? 64 : 1;
+  // fp32 layers run their expert GEMMs as split-bf16 tcgen05 GEMMs (one
+  // rank, widths the tcgen05 tiles take); MOE_F32_GEMM=simt keeps the FFMA path
+  {
+    const char* env = std::getenv("MOE_F32_GEMM");
+    split32 = dt == MOE_DTYPE_F32 && P == 1 && dm % 128 == 0 && dff % 128 == 0 &&
+              !(env && std::string(env) == "simt");
+  }
+  pad = (dt == MOE_DTYPE_BF16 || split32) ? 64 : 1;
   Cs = round_up(C ? C : 1, pad);
   rows = (uint64_t)P * El * Cs;
   Epad = (uint32_t)round_up(E, 64);
@@ -148,6 +155,20 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   gmk = dalloc<int32_t>(owned, E);
   gak = dalloc<int32_t>(owned, E);
   gbk = dalloc<int32_t>(owned, E);
+  if (split32) {
+    const uint64_t kc = 512;  // K chunk: bounds the truncating tensor-core accumulation
+    xr3 = dalloc_bytes(owned, 3 * rows * dm * 2);
+    dy3 = dalloc_bytes(owned, 3 * rows * dm * 2);
+    a3 = dalloc_bytes(owned, 3 * rows * dff * 2);
+    dh3 = dalloc_bytes(owned, 3 * rows * dff * 2);
+    w1_3 = dalloc_bytes(owned, 3 * (uint64_t)El * dff * dm * 2);
+    w2_3 = dalloc_bytes(owned, 3 * (uint64_t)El * dff * dm * 2);
+    const uint64_t np_m = std::max(ceil_div((uint64_t)dm, kc) * dff, ceil_div((uint64_t)dff, kc) * dm);
+    s_part = dalloc<float>(owned, std::max(np_m * rows, ceil_div(Cs, kc) * El * dff * dm));
+    s_cs = dalloc<float>(owned, colsum_ws_floats(ngroups, dff, Cs));
+    s_cm = dalloc<int32_t>(owned, E);
+    s_ca = dalloc<int32_t>(owned, E);
+  }
   Gp = dalloc_bytes(owned, rows * dff * esz);
   Aact = dalloc_bytes(owned, rows * dff * esz);
   Yl = dalloc_bytes(owned, slot_bytes);
@@ -238,6 +259,42 @@ RemoteRows Layer::remote_rows(uint64_t home_off) const {
   return r;
 }
 
+// One fp32 GEMM as split-bf16 tcgen05 GEMMs over K chunks of <= 512: p is
+// the problem on three-plane operands (split_terms = 6, fp32 STORE); chunk c
+// writes out_parts + c * part_stride.  RAGGED_M chunks K; RAGGED_K chunks each
+// group's rows (s_cm / s_ca tables).
+void Layer::split_gemm(moe_gemm_problem_t p, float* out_parts, uint64_t part_stride, int* nparts,
+                       cudaStream_t st) {
+  constexpr uint32_t kc = 512;
+  p.dtype_ab = MOE_DTYPE_BF16;
+  p.dtype_c = MOE_DTYPE_F32;
+  p.split_terms = 6;
+  p.epilogue = MOE_EPI_STORE;
+  p.bias = nullptr;
+  if (p.kind == MOE_GEMM_RAGGED_M) {
+    const int n = (int)ceil_div((uint64_t)p.K, (uint64_t)kc);
+    for (int c = 0; c < n; ++c) {
+      moe_gemm_problem_t q = p;
+      q.k_begin = c * kc;
+      q.k_len = std::min<uint32_t>(kc, p.K - c * kc);
+      q.C = out_parts + (uint64_t)c * part_stride;
+      grouped_gemm(q, st);
+    }
+    *nparts = n;
+  } else {
+    const int n = (int)ceil_div(Cs, (uint64_t)kc);
+    for (int c = 0; c < n; ++c) {
+      chunk_groups(p.groups, p.m, p.a_row, (int)kc, c, s_cm, s_ca, st);
+      moe_gemm_problem_t q = p;
+      q.m = s_cm;
+      q.a_row = s_ca;
+      q.C = out_parts + (uint64_t)c * part_stride;
+      grouped_gemm(q, st);
+    }
+    *nparts = n;
+  }
+}
+
 moe_gemm_problem_t Layer::expert_problem() const {
   moe_gemm_problem_t p;
   std::memset(&p, 0, sizeof(p));
@@ -322,6 +379,34 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   mark("a2a_dispatch", st);
   if (!p2p) build_groups(P, El, Cs, cnt_recv, gm, ga, gb, gmk, gak, gbk, st);
   // K5: H = X W1^T + b1 (stored), A = gelu(H); Y = A W2^T + b2
+  const bool fused_return = p2p && dt == MOE_DTYPE_BF16;
+  if (split32) {
+    const uint64_t wn = (uint64_t)El * dff * dm;
+    split_f32_bf16x3(static_cast<const float*>(xr), rows * dm, xr3, st);
+    split_f32_bf16x3(static_cast<const float*>(w.w1), wn, w1_3, st);
+    split_f32_bf16x3(static_cast<const float*>(w.w2), wn, w2_3, st);
+    int np = 0;
+    moe_gemm_problem_t p = expert_problem();
+    p.N = dff;
+    p.K = dm;
+    p.A = xr3;
+    p.B = w1_3;
+    p.ldc = dff;
+    split_gemm(p, s_part, rows * dff, &np, st);
+    split_finish(1, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)Cs, dff, w.b1, nullptr,
+                 static_cast<float*>(Aact), static_cast<float*>(Gp), st);
+    mark("ffn1", st);
+    split_f32_bf16x3(static_cast<const float*>(Aact), rows * dff, a3, st);
+    p = expert_problem();
+    p.N = dm;
+    p.K = dff;
+    p.A = a3;
+    p.B = w2_3;
+    p.ldc = dm;
+    split_gemm(p, s_part, rows * dm, &np, st);
+    split_finish(0, s_part, np, rows * dm, ngroups, gm, ga, gb, (uint32_t)Cs, dm, w.b2, nullptr,
+                 static_cast<float*>(Yl), nullptr, st);
+  } else {
   {
     moe_gemm_problem_t p = expert_problem();
     p.epilogue = MOE_EPI_GELU;
@@ -336,7 +421,6 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     grouped_gemm(p, st);
   }
   mark("ffn1", st);
-  const bool fused_return = p2p && dt == MOE_DTYPE_BF16;
   {
     moe_gemm_problem_t p = expert_problem();
     p.epilogue = MOE_EPI_STORE;
@@ -355,6 +439,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
       grouped_gemm(p, st);
     }
   }
+  }  // !split32
   mark("ffn2", st);
   if (p2p) {
     if (fused_return) p2p_signal(win, SLOT_Y, ph, st);
@@ -464,6 +549,27 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   // Weight-gradient GEMMs (RAGGED_K over the slices of each expert):
   // dW1[j] = sum dH^T X, dW2[j] = sum dY^T A.
   auto wgrad = [&](bool w1, cudaStream_t s) {
+    if (split32) {  // dW = sum over row chunks of split-bf16 RAGGED_K GEMMs
+      moe_gemm_problem_t p;
+      std::memset(&p, 0, sizeof(p));
+      p.kind = MOE_GEMM_RAGGED_K;
+      p.groups = ngroups;
+      p.a_rows = rows;
+      p.num_b = El;
+      p.m = gmk;
+      p.a_row = gak;
+      p.b = gbk;
+      p.M = w1 ? dff : dm;
+      p.N = w1 ? dm : dff;
+      p.A = w1 ? dh3 : dy3;
+      p.B = w1 ? xr3 : a3;
+      p.ldc = p.N;
+      const uint64_t wn = (uint64_t)El * dff * dm;
+      int np = 0;
+      split_gemm(p, s_part, wn, &np, s);
+      sum_parts(s_part, np, wn, 1, wn, wn, false, static_cast<float*>(w1 ? g.dw1 : g.dw2), s);
+      return;
+    }
     moe_gemm_problem_t p;
     std::memset(&p, 0, sizeof(p));
     p.kind = MOE_GEMM_RAGGED_K;
@@ -496,6 +602,34 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   // K5^T dgrad: dH = (dY W2) * gelu'(h) (stored by ffn1), db1 = column sums
   // of dH fused into the same epilogue (per-block partials, fixed-order sum);
   // dXe = dH W1
+  const bool fused_return = p2p && dt == MOE_DTYPE_BF16;
+  if (split32) {
+    int np = 0;
+    split_f32_bf16x3(static_cast<const float*>(dYr), rows * dm, dy3, st);
+    moe_gemm_problem_t p = expert_problem();
+    p.b_mn_major = 1;
+    p.N = dff;
+    p.K = dm;
+    p.A = dy3;
+    p.B = w2_3;
+    p.ldc = dff;
+    split_gemm(p, s_part, rows * dff, &np, st);
+    split_finish(2, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)Cs, dff, nullptr,
+                 static_cast<const float*>(Gp), static_cast<float*>(dH), nullptr, st);
+    group_colsum(ngroups, gm, ga, gb, El, dff, dt, dH, g.db1, st, Cs, s_cs, nullptr);
+    mark("dgrad_ffn2", st);
+    split_f32_bf16x3(static_cast<const float*>(dH), rows * dff, dh3, st);
+    p = expert_problem();
+    p.b_mn_major = 1;
+    p.N = dm;
+    p.K = dff;
+    p.A = dh3;
+    p.B = w1_3;
+    p.ldc = dm;
+    split_gemm(p, s_part, rows * dm, &np, st);
+    split_finish(0, s_part, np, rows * dm, ngroups, gm, ga, gb, (uint32_t)Cs, dm, nullptr, nullptr,
+                 static_cast<float*>(dXl), nullptr, st);
+  } else {
   {
     moe_gemm_problem_t p = expert_problem();
     p.epilogue = MOE_EPI_DGELU;
@@ -513,7 +647,6 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     grouped_gemm(p, st);
   }
   mark("dgrad_ffn2", st);
-  const bool fused_return = p2p && dt == MOE_DTYPE_BF16;
   {
     moe_gemm_problem_t p = expert_problem();
     p.epilogue = MOE_EPI_STORE;
@@ -531,6 +664,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
       grouped_gemm(p, st);
     }
   }
+  }  // !split32
   mark("dgrad_ffn1", st);
   if (p2p) {
     if (fused_return) p2p_signal(win, SLOT_DX, ph, st);

@@ -83,6 +83,16 @@ struct Layer {
   int32_t* gate_tab = nullptr;
   int32_t *split_m = nullptr, *split_a = nullptr, *split_b = nullptr;
   uint32_t nsplit = 1;
+  // fp32 expert GEMMs on the bf16 tensor cores (f32split.cu): three bf16
+  // planes per operand, K-chunk partials summed in fp32 by split_finish
+  bool split32 = false;
+  void *xr3 = nullptr, *a3 = nullptr, *dy3 = nullptr, *dh3 = nullptr, *w1_3 = nullptr,
+       *w2_3 = nullptr;
+  float* s_part = nullptr;        // K-chunk partials
+  float* s_cs = nullptr;          // db1 column-sum chunk partials (N = d_ff)
+  int32_t *s_cm = nullptr, *s_ca = nullptr;  // row-chunk group tables of the weight gradients
+  void split_gemm(moe_gemm_problem_t p, float* out_parts, uint64_t part_stride, int* nparts,
+                  cudaStream_t st);
   const void* x_saved_ptr = nullptr;
   void* x_stage = nullptr;          // host-buffer pipeline: 2 x (x, dy, y, dx)
   cudaStream_t hp_stream[3] = {};   // h2d, compute, d2h

@@ -266,3 +266,77 @@ def test_tc_many_groups_persistent_schedule():
     got, ref, _, _ = ragged_m_case(torch.bfloat16, False, _lib.MOE_EPI_STORE, N=1024, K=128,
                                    groups=groups, bvec=bvec, Cs=320)
     assert_close(got, ref, 1e-2)
+
+
+def _split3(x):
+    from paper_2205_10034_b200._lib import call
+    x = x.contiguous()
+    out = torch.empty(3 * x.numel(), dtype=torch.bfloat16, device=x.device)
+    call("moe_split_f32_bf16x3", x.data_ptr(), x.numel(), out.data_ptr(),
+         torch.cuda.current_stream().cuda_stream)
+    return out
+
+
+def test_split_f32_planes_exact():
+    x = (torch.randn(4096, device=dev) * torch.logspace(-20, 20, 4096, device=dev)).float()
+    p = _split3(x).view(3, -1).double()
+    assert torch.equal(p.sum(0), x.double())
+
+
+@pytest.mark.parametrize("b_mn", [False, True])
+def test_split_f32_ragged_m_chunked(b_mn):
+    """fp32 GEMM as six split-bf16 plane products on tcgen05, K chunks of 512
+    summed in fp32: ~fp32 accuracy (the c1 path) vs an fp64 reference."""
+    G, rows, N, K = 3, 300, 256, 1024
+    torch.manual_seed(1)
+    A = torch.randn(G * rows, K, device=dev)
+    W = torch.randn(G, N, K, device=dev) / K ** 0.5
+    Bst = W.transpose(1, 2).contiguous() if b_mn else W.contiguous()
+    A3, B3 = _split3(A), _split3(Bst)
+    m, ar, b = i32([rows, 0, 171]), i32([g * rows for g in range(G)]), i32([0, 1, 2])
+    parts = torch.zeros(2, G * rows, N, device=dev)
+    for c in range(2):
+        p = GemmProblem()
+        p.kind, p.epilogue = _lib.MOE_GEMM_RAGGED_M, _lib.MOE_EPI_STORE
+        p.dtype_ab, p.dtype_c = _lib.MOE_DTYPE_BF16, _lib.MOE_DTYPE_F32
+        p.b_mn_major = 1 if b_mn else 0
+        p.groups, p.N, p.K, p.a_rows, p.num_b = G, N, K, G * rows, G
+        p.m, p.a_row, p.c_row, p.b = m.data_ptr(), ar.data_ptr(), ar.data_ptr(), b.data_ptr()
+        p.A, p.B, p.C = A3.data_ptr(), B3.data_ptr(), parts[c].data_ptr()
+        p.ldc, p.split_terms, p.k_begin, p.k_len = N, 6, 512 * c, 512
+        grouped_gemm(p)
+    torch.cuda.synchronize()
+    got = parts.sum(0).double()
+    for g, mm in enumerate([rows, 0, 171]):
+        if mm == 0:
+            continue
+        r0 = g * rows
+        ref = A[r0:r0 + mm].double() @ W[g].double().t()
+        err = (got[r0:r0 + mm] - ref).abs().max() / ref.abs().max()
+        assert err < 2e-6, (g, err.item())
+
+
+def test_split_f32_ragged_k():
+    G, rows, M, N = 2, 448, 256, 128
+    torch.manual_seed(2)
+    A = torch.randn(G * rows, M, device=dev)
+    B = torch.randn(G * rows, N, device=dev)
+    m = [rows, 300]
+    for g, mm in enumerate(m):  # rows past m up to the next 64 are zero
+        A[g * rows + mm:(g + 1) * rows] = 0
+        B[g * rows + mm:(g + 1) * rows] = 0
+    A3, B3 = _split3(A), _split3(B)
+    C = torch.zeros(G, M, N, device=dev)
+    p = GemmProblem()
+    p.kind, p.epilogue = _lib.MOE_GEMM_RAGGED_K, _lib.MOE_EPI_STORE
+    p.dtype_ab, p.dtype_c = _lib.MOE_DTYPE_BF16, _lib.MOE_DTYPE_F32
+    p.groups, p.M, p.N, p.a_rows, p.num_b = G, M, N, G * rows, G
+    mt, at, bt = i32(m), i32([0, rows]), i32([0, 1])
+    p.m, p.a_row, p.b = mt.data_ptr(), at.data_ptr(), bt.data_ptr()
+    p.A, p.B, p.C, p.ldc, p.split_terms = A3.data_ptr(), B3.data_ptr(), C.data_ptr(), N, 6
+    grouped_gemm(p)
+    torch.cuda.synchronize()
+    for g in range(G):
+        ref = A[g * rows:(g + 1) * rows].double().t() @ B[g * rows:(g + 1) * rows].double()
+        err = (C[g].double() - ref).abs().max() / ref.abs().max()
+        assert err < 2e-6, (g, err.item())
