@@ -231,6 +231,8 @@ typedef struct moe_gemm_problem {
   uint32_t split_terms;   /* 0 or 1: plain; 6: split-fp32                                */
   uint32_t k_begin;       /* RAGGED_M: K sub-range [k_begin, k_begin + k_len) (multiples */
   uint32_t k_len;         /*   of 64; k_len 0 = to K) -- bounds accumulation chains      */
+  const int32_t* k_begin_g; /* RAGGED_M, nullable: per-group K start (overrides k_begin;
+                               with c_row, one launch computes every K chunk's partial) */
 } moe_gemm_problem_t;
 
 moe_status_t moe_grouped_gemm(const moe_gemm_problem_t* problem, void* stream);

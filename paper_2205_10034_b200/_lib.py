@@ -120,6 +120,7 @@ class GemmProblem(C.Structure):
         ("split_terms", C.c_uint32),
         ("k_begin", C.c_uint32),
         ("k_len", C.c_uint32),
+        ("k_begin_g", C.c_void_p),
     ]
 
 

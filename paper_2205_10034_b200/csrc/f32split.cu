@@ -21,32 +21,39 @@
 namespace moe {
 namespace {
 
+__device__ __forceinline__ void split3_store4(float4 v, __nv_bfloat16* out, uint64_t n,
+                                              uint64_t at) {
+  const float x[4] = {v.x, v.y, v.z, v.w};
+  uint32_t w[3][2];
+#pragma unroll
+  for (int j = 0; j < 4; j += 2) {
+    uint32_t lo[3], hi[3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const __nv_bfloat16 a = __float2bfloat16_rn(x[j + h]);
+      const float r1 = x[j + h] - __bfloat162float(a);  // exact
+      const __nv_bfloat16 b = __float2bfloat16_rn(r1);
+      const __nv_bfloat16 c = __float2bfloat16_rn(r1 - __bfloat162float(b));
+      const uint32_t ua = __bfloat16_as_ushort(a), ub = __bfloat16_as_ushort(b),
+                     uc = __bfloat16_as_ushort(c);
+      if (h == 0) { lo[0] = ua; lo[1] = ub; lo[2] = uc; }
+      else { hi[0] = ua; hi[1] = ub; hi[2] = uc; }
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) w[t][j / 2] = lo[t] | (hi[t] << 16);
+  }
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+    *reinterpret_cast<uint2*>(out + (uint64_t)t * n + at) = make_uint2(w[t][0], w[t][1]);
+}
+
 __global__ void split3_kernel(const float* __restrict__ in, uint64_t n4,
                               __nv_bfloat16* __restrict__ out, uint64_t n) {
   pdl_wait();
   pdl_trigger();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(in) + i);
-    const float x[4] = {v.x, v.y, v.z, v.w};
-    __nv_bfloat16 p[3][4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const __nv_bfloat16 a = __float2bfloat16_rn(x[j]);
-      const float r1 = x[j] - __bfloat162float(a);  // exact (Sterbenz)
-      const __nv_bfloat16 b = __float2bfloat16_rn(r1);
-      const __nv_bfloat16 c = __float2bfloat16_rn(r1 - __bfloat162float(b));
-      p[0][j] = a;
-      p[1][j] = b;
-      p[2][j] = c;
-    }
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-      uint2 w;
-      w.x = (uint32_t)__bfloat16_as_ushort(p[t][0]) | ((uint32_t)__bfloat16_as_ushort(p[t][1]) << 16);
-      w.y = (uint32_t)__bfloat16_as_ushort(p[t][2]) | ((uint32_t)__bfloat16_as_ushort(p[t][3]) << 16);
-      *reinterpret_cast<uint2*>(out + (uint64_t)t * n + 4 * i) = w;
-    }
+    split3_store4(__ldg(reinterpret_cast<const float4*>(in) + i), out, n, 4 * i);
   }
 }
 
@@ -54,13 +61,16 @@ __global__ void split3_kernel(const float* __restrict__ in, uint64_t n4,
 //   h = sum_c part[c][row][n] (+ bias[gb[g]][n]); MODE 0: out = h;
 //   MODE 1: out = gelu(h), out2 = gelu'(h); MODE 2: out = h * aux[row][n];
 // rows in [gm[g], stride) are zeroed (the tcgen05 RAGGED_K GEMMs read whole
-// 64-row K blocks).  Grid: (groups, row blocks of 8, column blocks of 128).
+// 64-row K blocks).  out3 (nullable): the result's three bf16 planes too (the
+// next split GEMM's operand; n3 = elements per plane) -- for MODE 1 it
+// replaces out (the fp32 activation itself is never read again).
+// Grid: (groups, row blocks of 8, column blocks of 128).
 template <int MODE>
 __global__ void __launch_bounds__(256) finish_kernel(
     const float* __restrict__ part, int nparts, uint64_t pstride, const int32_t* __restrict__ gm,
     const int32_t* __restrict__ ga, const int32_t* __restrict__ gb, int stride, int N,
     const float* __restrict__ bias, const float* __restrict__ aux, float* __restrict__ out,
-    float* __restrict__ out2) {
+    float* __restrict__ out2, __nv_bfloat16* __restrict__ out3, uint64_t n3) {
   pdl_wait();
   pdl_trigger();
   const int g = blockIdx.x;
@@ -94,7 +104,8 @@ __global__ void __launch_bounds__(256) finish_kernel(
     gelu_and_grad_f(h.z, a.z, d.z);
     gelu_and_grad_f(h.w, a.w, d.w);
     if (r >= m) a = d = make_float4(0.f, 0.f, 0.f, 0.f);
-    *reinterpret_cast<float4*>(out + off) = a;
+    if (out) *reinterpret_cast<float4*>(out + off) = a;
+    if (out3) split3_store4(a, out3, n3, off);
     *reinterpret_cast<float4*>(out2 + off) = d;
     return;
   }
@@ -105,18 +116,35 @@ __global__ void __launch_bounds__(256) finish_kernel(
     h.z *= x.z;
     h.w *= x.w;
   }
-  *reinterpret_cast<float4*>(out + off) = h;
+  if (out) *reinterpret_cast<float4*>(out + off) = h;
+  if (out3) split3_store4(h, out3, n3, off);
 }
 
-__global__ void chunk_groups_kernel(uint32_t groups, const int32_t* __restrict__ gm,
-                                    const int32_t* __restrict__ ga, int chunk, int c,
-                                    int32_t* __restrict__ cm, int32_t* __restrict__ ca) {
+// K-chunk group tables, group (c, g) = c * groups + g:
+//   RAGGED_M (kind 0): m = gm, a_row = ga, c_row = c * rows + ga, b = gb, k = c * chunk
+//   RAGGED_K (kind 1): m = clamp(gm - c*chunk, 0, chunk), a_row = ga + c*chunk, b = c*nb + gb
+__global__ void chunk_tables_kernel(int kind, uint32_t groups, int nchunks, int chunk, int rows,
+                                    int nb, const int32_t* __restrict__ gm,
+                                    const int32_t* __restrict__ ga, const int32_t* __restrict__ gb,
+                                    int32_t* __restrict__ om, int32_t* __restrict__ oa,
+                                    int32_t* __restrict__ oc, int32_t* __restrict__ ob,
+                                    int32_t* __restrict__ ok) {
   pdl_wait();
   pdl_trigger();
-  const uint32_t g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= groups) return;
-  cm[g] = max(0, min(chunk, gm[g] - c * chunk));
-  ca[g] = ga[g] + c * chunk;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= groups * (uint32_t)nchunks) return;
+  const int c = (int)(i / groups), g = (int)(i % groups);
+  if (kind == 0) {
+    om[i] = gm[g];
+    oa[i] = ga[g];
+    oc[i] = c * rows + ga[g];
+    ob[i] = gb[g];
+    ok[i] = c * chunk;
+  } else {
+    om[i] = max(0, min(chunk, gm[g] - c * chunk));
+    oa[i] = ga[g] + c * chunk;
+    ob[i] = c * nb + gb[g];
+  }
 }
 
 }  // namespace
@@ -136,28 +164,31 @@ void split_f32_bf16x3(const float* in, uint64_t n, void* out, cudaStream_t st) {
 void split_finish(int mode, const float* part, int nparts, uint64_t part_stride, uint32_t groups,
                   const int32_t* gm, const int32_t* ga, const int32_t* gb, uint32_t stride,
                   uint32_t N, const float* bias, const float* aux, float* out, float* out2,
-                  cudaStream_t st) {
+                  void* out3, uint64_t n3, cudaStream_t st) {
+  __nv_bfloat16* o3 = static_cast<__nv_bfloat16*>(out3);
   arg_check(N % 4 == 0, "split_finish: N % 4 == 0 required");
   const dim3 grid(groups, (unsigned)ceil_div((uint64_t)stride, (uint64_t)8),
                   (unsigned)ceil_div((uint64_t)N, (uint64_t)128));
   if (mode == 0)
     launch_pdl(finish_kernel<0>, grid, 256, 0, st, part, nparts, part_stride, gm, ga, gb,
-               (int)stride, (int)N, bias, aux, out, out2);
+               (int)stride, (int)N, bias, aux, out, out2, o3, n3);
   else if (mode == 1)
     launch_pdl(finish_kernel<1>, grid, 256, 0, st, part, nparts, part_stride, gm, ga, gb,
-               (int)stride, (int)N, bias, aux, out, out2);
+               (int)stride, (int)N, bias, aux, out, out2, o3, n3);
   else
     launch_pdl(finish_kernel<2>, grid, 256, 0, st, part, nparts, part_stride, gm, ga, gb,
-               (int)stride, (int)N, bias, aux, out, out2);
+               (int)stride, (int)N, bias, aux, out, out2, o3, n3);
   MOE_LAUNCH_CHECK("finish_kernel");
   count_launch();
 }
 
-void chunk_groups(uint32_t groups, const int32_t* gm, const int32_t* ga, int chunk, int c,
-                  int32_t* cm, int32_t* ca, cudaStream_t st) {
-  launch_pdl(chunk_groups_kernel, (unsigned)ceil_div((uint64_t)groups, (uint64_t)256), 256, 0, st,
-             groups, gm, ga, chunk, c, cm, ca);
-  MOE_LAUNCH_CHECK("chunk_groups_kernel");
+void chunk_tables(int kind, uint32_t groups, int nchunks, int chunk, int rows, int nb,
+                  const int32_t* gm, const int32_t* ga, const int32_t* gb, int32_t* om,
+                  int32_t* oa, int32_t* oc, int32_t* ob, int32_t* ok, cudaStream_t st) {
+  const uint64_t n = (uint64_t)groups * nchunks;
+  launch_pdl(chunk_tables_kernel, (unsigned)ceil_div(n, (uint64_t)256), 256, 0, st, kind, groups,
+             nchunks, chunk, rows, nb, gm, ga, gb, om, oa, oc, ob, ok);
+  MOE_LAUNCH_CHECK("chunk_tables_kernel");
   count_launch();
 }
 

@@ -113,6 +113,7 @@ struct Args {
   int terms;
   long long a_plane, b_plane;
   int k_begin, k_len;
+  const int* gkb;  // RAGGED_M: per-group K start (nullable: k_begin for all)
 };
 
 // plane pairs of the split-fp32 products, smallest first: the tensor core's
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const int arow = args.ga[g] + mb * TM + (int)crank * (is_tail(g, mb) ? 64 : BM);
           const int brow = args.gb[g] * (B_MN ? args.K : args.N);
           const int bcol = nb * BN + (int)crank * BH;
-          const int nk = args.k_len / BK, kb0 = args.k_begin / BK;
+          const int nk = args.k_len / BK, kb0 = (args.gkb ? args.gkb[g] : args.k_begin) / BK;
           const int nkb = nk * args.terms;
           for (int i = 0; i < nkb; ++i, ++it) {
             const int t = args.terms == 1 ? 0 : i / nk;
@@ -936,6 +937,7 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   a.b_plane = (long long)b_plane;
   a.k_begin = (int)p.k_begin;
   a.k_len = (int)(p.k_len ? p.k_len : p.K - p.k_begin);
+  a.gkb = p.k_begin_g;
   RemoteOut ro;  // remote descriptor (copied into the launch parameters)
   std::memset(&ro, 0, sizeof(ro));
   if (REMOTE) {
@@ -1003,6 +1005,8 @@ void tc_grouped_gemm(const moe_gemm_problem_t& p, cudaStream_t st, const RemoteR
   arg_check(p.kind == MOE_GEMM_RAGGED_K ||
                 (p.k_begin % BK == 0 && p.k_len % BK == 0 && p.k_begin + p.k_len <= p.K),
             "gemm.k_begin/k_len: multiples of 64 inside [0, K]");
+  arg_check(!p.k_begin_g || (p.kind == MOE_GEMM_RAGGED_M && p.k_len > 0),
+            "gemm.k_begin_g: per-group K starts need RAGGED_M and k_len");
   const bool f32 = p.dtype_c == MOE_DTYPE_F32;
   if (p.kind == MOE_GEMM_RAGGED_M) {
     arg_check(p.K % BK == 0, "gemm.K: must be a multiple of 64");

@@ -138,10 +138,14 @@ void split_f32_bf16x3(const float* in, uint64_t n, void* out, cudaStream_t st);
 void split_finish(int mode, const float* part, int nparts, uint64_t part_stride, uint32_t groups,
                   const int32_t* gm, const int32_t* ga, const int32_t* gb, uint32_t stride,
                   uint32_t N, const float* bias, const float* aux, float* out, float* out2,
-                  cudaStream_t st);
-// row chunk c of every group: cm = clamp(m - c*chunk, 0, chunk), ca = a_row + c*chunk
-void chunk_groups(uint32_t groups, const int32_t* gm, const int32_t* ga, int chunk, int c,
-                  int32_t* cm, int32_t* ca, cudaStream_t st);
+                  void* out3 = nullptr, uint64_t n3 = 0, cudaStream_t st = nullptr);
+// K-chunk group tables (group (c, g) = c*groups + g): RAGGED_M (kind 0) keeps
+// the rows and sets c_row = c*rows + a_row, k = c*chunk; RAGGED_K (kind 1) cuts
+// every group's rows into chunks: m = clamp(m - c*chunk, 0, chunk), a_row +=
+// c*chunk, output b = c*nb + b.  oc / ok unused (nullable) for kind 1.
+void chunk_tables(int kind, uint32_t groups, int nchunks, int chunk, int rows, int nb,
+                  const int32_t* gm, const int32_t* ga, const int32_t* gb, int32_t* om,
+                  int32_t* oa, int32_t* oc, int32_t* ob, int32_t* ok, cudaStream_t st);
 
 // Round-robin placement relabel (include/moe_b200.h): pexpert = pi(expert),
 // pkept[pi(e)] = kept[e], pi(e) = (e % P) * (E / P) + e / P.

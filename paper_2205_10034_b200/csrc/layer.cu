@@ -19,6 +19,8 @@
 #include <nccl.h>
 
 #include <cstdlib>
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -92,6 +94,18 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
               !(env && std::string(env) == "simt");
   }
   pad = (dt == MOE_DTYPE_BF16 || split32) ? 64 : 1;
+  if (split32) {  // one launch holds every K chunk: groups x chunks <= 1024 tile groups
+    auto nchunks = [](uint64_t K) {
+      uint64_t n = 1;
+      while (K / n > 512 || (K / 64) % n) ++n;
+      return n;
+    };
+    const uint64_t cs = round_up((uint64_t)std::ceil((double)k * d.capacity_factor * (double)T /
+                                                     (double)E), 64);
+    const uint64_t nmax =
+        std::max({nchunks(dm), nchunks(dff), ceil_div(std::max<uint64_t>(cs, 1), (uint64_t)512)});
+    split32 = nmax <= 64 && (uint64_t)E * nmax <= 1024;
+  }
   Cs = round_up(C ? C : 1, pad);
   rows = (uint64_t)P * El * Cs;
   Epad = (uint32_t)round_up(E, 64);
@@ -166,8 +180,12 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
     const uint64_t np_m = std::max(ceil_div((uint64_t)dm, kc) * dff, ceil_div((uint64_t)dff, kc) * dm);
     s_part = dalloc<float>(owned, std::max(np_m * rows, ceil_div(Cs, kc) * El * dff * dm));
     s_cs = dalloc<float>(owned, colsum_ws_floats(ngroups, dff, Cs));
-    s_cm = dalloc<int32_t>(owned, E);
-    s_ca = dalloc<int32_t>(owned, E);
+    const uint64_t nt = (uint64_t)E * 64;  // groups x K chunks (chunks <= 64)
+    s_tm = dalloc<int32_t>(owned, nt);
+    s_ta = dalloc<int32_t>(owned, nt);
+    s_tc = dalloc<int32_t>(owned, nt);
+    s_tb = dalloc<int32_t>(owned, nt);
+    s_tk = dalloc<int32_t>(owned, nt);
   }
   Gp = dalloc_bytes(owned, rows * dff * esz);
   Aact = dalloc_bytes(owned, rows * dff * esz);
@@ -259,40 +277,50 @@ RemoteRows Layer::remote_rows(uint64_t home_off) const {
   return r;
 }
 
-// One fp32 GEMM as split-bf16 tcgen05 GEMMs over K chunks of <= 512: p is
-// the problem on three-plane operands (split_terms = 6, fp32 STORE); chunk c
-// writes out_parts + c * part_stride.  RAGGED_M chunks K; RAGGED_K chunks each
-// group's rows (s_cm / s_ca tables).
+// One fp32 GEMM as split-bf16 tcgen05 GEMMs over K chunks of <= 512, all
+// chunks in ONE launch (group (c, g) writes partial c): p is the problem on
+// three-plane operands; partial c lands at out_parts + c * part_stride.
+// RAGGED_M: K cut into n equal 64-multiples (per-group k_begin_g, c_row =
+// c * rows + a_row); RAGGED_K: every group's rows cut at 512 (output c*El+b).
 void Layer::split_gemm(moe_gemm_problem_t p, float* out_parts, uint64_t part_stride, int* nparts,
                        cudaStream_t st) {
-  constexpr uint32_t kc = 512;
   p.dtype_ab = MOE_DTYPE_BF16;
   p.dtype_c = MOE_DTYPE_F32;
   p.split_terms = 6;
   p.epilogue = MOE_EPI_STORE;
   p.bias = nullptr;
+  p.C = out_parts;
+  const uint32_t G = p.groups;
   if (p.kind == MOE_GEMM_RAGGED_M) {
-    const int n = (int)ceil_div((uint64_t)p.K, (uint64_t)kc);
-    for (int c = 0; c < n; ++c) {
-      moe_gemm_problem_t q = p;
-      q.k_begin = c * kc;
-      q.k_len = std::min<uint32_t>(kc, p.K - c * kc);
-      q.C = out_parts + (uint64_t)c * part_stride;
-      grouped_gemm(q, st);
-    }
-    *nparts = n;
+    const uint32_t kb = p.K / 64;
+    uint32_t n = 1;
+    while (p.K / n > 512 || kb % n) ++n;
+    const uint32_t chunk = p.K / n;
+    chunk_tables(0, G, (int)n, (int)chunk, (int)rows, (int)p.num_b, p.m, p.a_row, p.b, s_tm, s_ta,
+                 s_tc, s_tb, s_tk, st);
+    arg_check(part_stride == rows * (uint64_t)p.N, "split_gemm: RAGGED_M partial stride");
+    p.groups = G * n;
+    p.m = s_tm;
+    p.a_row = s_ta;
+    p.c_row = s_tc;
+    p.b = s_tb;
+    p.k_begin_g = s_tk;
+    p.k_len = chunk;
+    p.c_rows = n * rows;
+    *nparts = (int)n;
   } else {
-    const int n = (int)ceil_div(Cs, (uint64_t)kc);
-    for (int c = 0; c < n; ++c) {
-      chunk_groups(p.groups, p.m, p.a_row, (int)kc, c, s_cm, s_ca, st);
-      moe_gemm_problem_t q = p;
-      q.m = s_cm;
-      q.a_row = s_ca;
-      q.C = out_parts + (uint64_t)c * part_stride;
-      grouped_gemm(q, st);
-    }
-    *nparts = n;
+    const uint32_t n = (uint32_t)ceil_div(Cs, (uint64_t)512);
+    chunk_tables(1, G, (int)n, 512, (int)rows, (int)p.num_b, p.m, p.a_row, p.b, s_tm, s_ta,
+                 nullptr, s_tb, nullptr, st);
+    arg_check(part_stride == (uint64_t)p.num_b * p.M * p.N, "split_gemm: RAGGED_K partial stride");
+    p.groups = G * n;
+    p.m = s_tm;
+    p.a_row = s_ta;
+    p.b = s_tb;
+    p.num_b *= n;
+    *nparts = (int)n;
   }
+  grouped_gemm(p, st);
 }
 
 moe_gemm_problem_t Layer::expert_problem() const {
@@ -393,10 +421,10 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     p.B = w1_3;
     p.ldc = dff;
     split_gemm(p, s_part, rows * dff, &np, st);
+    // A = gelu(h) goes straight to its bf16 planes (ffn2's and wgrad-w2's operand)
     split_finish(1, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)Cs, dff, w.b1, nullptr,
-                 static_cast<float*>(Aact), static_cast<float*>(Gp), st);
+                 nullptr, static_cast<float*>(Gp), a3, rows * dff, st);
     mark("ffn1", st);
-    split_f32_bf16x3(static_cast<const float*>(Aact), rows * dff, a3, st);
     p = expert_problem();
     p.N = dm;
     p.K = dff;
@@ -405,7 +433,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     p.ldc = dm;
     split_gemm(p, s_part, rows * dm, &np, st);
     split_finish(0, s_part, np, rows * dm, ngroups, gm, ga, gb, (uint32_t)Cs, dm, w.b2, nullptr,
-                 static_cast<float*>(Yl), nullptr, st);
+                 static_cast<float*>(Yl), nullptr, nullptr, 0, st);
   } else {
   {
     moe_gemm_problem_t p = expert_problem();
@@ -615,10 +643,10 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.ldc = dff;
     split_gemm(p, s_part, rows * dff, &np, st);
     split_finish(2, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)Cs, dff, nullptr,
-                 static_cast<const float*>(Gp), static_cast<float*>(dH), nullptr, st);
+                 static_cast<const float*>(Gp), static_cast<float*>(dH), nullptr, dh3, rows * dff,
+                 st);
     group_colsum(ngroups, gm, ga, gb, El, dff, dt, dH, g.db1, st, Cs, s_cs, nullptr);
     mark("dgrad_ffn2", st);
-    split_f32_bf16x3(static_cast<const float*>(dH), rows * dff, dh3, st);
     p = expert_problem();
     p.b_mn_major = 1;
     p.N = dm;
@@ -628,7 +656,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.ldc = dm;
     split_gemm(p, s_part, rows * dm, &np, st);
     split_finish(0, s_part, np, rows * dm, ngroups, gm, ga, gb, (uint32_t)Cs, dm, nullptr, nullptr,
-                 static_cast<float*>(dXl), nullptr, st);
+                 static_cast<float*>(dXl), nullptr, nullptr, 0, st);
   } else {
   {
     moe_gemm_problem_t p = expert_problem();

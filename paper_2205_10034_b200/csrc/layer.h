@@ -90,7 +90,8 @@ struct Layer {
        *w2_3 = nullptr;
   float* s_part = nullptr;        // K-chunk partials
   float* s_cs = nullptr;          // db1 column-sum chunk partials (N = d_ff)
-  int32_t *s_cm = nullptr, *s_ca = nullptr;  // row-chunk group tables of the weight gradients
+  // K-chunk group tables (m, a_row, c_row, b, k) of one split-fp32 GEMM launch
+  int32_t *s_tm = nullptr, *s_ta = nullptr, *s_tc = nullptr, *s_tb = nullptr, *s_tk = nullptr;
   void split_gemm(moe_gemm_problem_t p, float* out_parts, uint64_t part_stride, int* nparts,
                   cudaStream_t st);
   const void* x_saved_ptr = nullptr;
