@@ -181,11 +181,13 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
     s_part = dalloc<float>(owned, std::max(np_m * rows, ceil_div(Cs, kc) * El * dff * dm));
     s_cs = dalloc<float>(owned, colsum_ws_floats(ngroups, dff, Cs));
     const uint64_t nt = (uint64_t)E * 64;  // groups x K chunks (chunks <= 64)
-    s_tm = dalloc<int32_t>(owned, nt);
-    s_ta = dalloc<int32_t>(owned, nt);
-    s_tc = dalloc<int32_t>(owned, nt);
-    s_tb = dalloc<int32_t>(owned, nt);
-    s_tk = dalloc<int32_t>(owned, nt);
+    for (auto& t : s_tab) {
+      t.m = dalloc<int32_t>(owned, nt);
+      t.a = dalloc<int32_t>(owned, nt);
+      t.c = dalloc<int32_t>(owned, nt);
+      t.b = dalloc<int32_t>(owned, nt);
+      t.k = dalloc<int32_t>(owned, nt);
+    }
   }
   Gp = dalloc_bytes(owned, rows * dff * esz);
   Aact = dalloc_bytes(owned, rows * dff * esz);
@@ -291,32 +293,45 @@ void Layer::split_gemm(moe_gemm_problem_t p, float* out_parts, uint64_t part_str
   p.bias = nullptr;
   p.C = out_parts;
   const uint32_t G = p.groups;
+  // this forward's tables for (kind, chunks), built on first use
+  auto tables = [&](int kind, uint32_t n, uint32_t chunk) -> ChunkTables& {
+    const int key = kind * 4096 + (int)n * 64 + (int)(chunk / 64);
+    ChunkTables* slot = &s_tab[0];
+    for (auto& t : s_tab) {
+      if (t.key == key && t.step == fwd_step) return t;
+      if (t.step != fwd_step || t.key < 0) slot = &t;
+    }
+    chunk_tables(kind, G, (int)n, (int)chunk, (int)rows, (int)p.num_b, p.m, p.a_row, p.b, slot->m,
+                 slot->a, kind == 0 ? slot->c : nullptr, slot->b, kind == 0 ? slot->k : nullptr,
+                 st);
+    slot->key = key;
+    slot->step = fwd_step;
+    return *slot;
+  };
   if (p.kind == MOE_GEMM_RAGGED_M) {
     const uint32_t kb = p.K / 64;
     uint32_t n = 1;
     while (p.K / n > 512 || kb % n) ++n;
     const uint32_t chunk = p.K / n;
-    chunk_tables(0, G, (int)n, (int)chunk, (int)rows, (int)p.num_b, p.m, p.a_row, p.b, s_tm, s_ta,
-                 s_tc, s_tb, s_tk, st);
+    const ChunkTables& t = tables(0, n, chunk);
     arg_check(part_stride == rows * (uint64_t)p.N, "split_gemm: RAGGED_M partial stride");
     p.groups = G * n;
-    p.m = s_tm;
-    p.a_row = s_ta;
-    p.c_row = s_tc;
-    p.b = s_tb;
-    p.k_begin_g = s_tk;
+    p.m = t.m;
+    p.a_row = t.a;
+    p.c_row = t.c;
+    p.b = t.b;
+    p.k_begin_g = t.k;
     p.k_len = chunk;
     p.c_rows = n * rows;
     *nparts = (int)n;
   } else {
     const uint32_t n = (uint32_t)ceil_div(Cs, (uint64_t)512);
-    chunk_tables(1, G, (int)n, 512, (int)rows, (int)p.num_b, p.m, p.a_row, p.b, s_tm, s_ta,
-                 nullptr, s_tb, nullptr, st);
+    const ChunkTables& t = tables(1, n, 512);
     arg_check(part_stride == (uint64_t)p.num_b * p.M * p.N, "split_gemm: RAGGED_K partial stride");
     p.groups = G * n;
-    p.m = s_tm;
-    p.a_row = s_ta;
-    p.b = s_tb;
+    p.m = t.m;
+    p.a_row = t.a;
+    p.b = t.b;
     p.num_b *= n;
     *nparts = (int)n;
   }
@@ -348,6 +363,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   x_saved_ptr = x;
   if (profiling) MOE_CUDA(cudaEventRecord(ev[0], st));
   const uint64_t ph = ++phase;
+  ++fwd_step;  // new group tables this step: the split-fp32 chunk tables go stale
   if (p2p) p2p_wait(win, SLOT_PHASE, ph - 1, st);  // peers done reading our previous writes
   // K1: logits = x wg^T (+ bg), fp32 out
   if (override_logits) {

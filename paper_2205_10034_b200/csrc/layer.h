@@ -90,8 +90,15 @@ struct Layer {
        *w2_3 = nullptr;
   float* s_part = nullptr;        // K-chunk partials
   float* s_cs = nullptr;          // db1 column-sum chunk partials (N = d_ff)
-  // K-chunk group tables (m, a_row, c_row, b, k) of one split-fp32 GEMM launch
-  int32_t *s_tm = nullptr, *s_ta = nullptr, *s_tc = nullptr, *s_tb = nullptr, *s_tk = nullptr;
+  // K-chunk group tables (m, a_row, c_row, b, k) of the split-fp32 GEMM
+  // launches, built once per forward (the group tables are fixed by then) for
+  // each (kind, chunks) shape: 4 slots
+  struct ChunkTables {
+    int32_t *m = nullptr, *a = nullptr, *c = nullptr, *b = nullptr, *k = nullptr;
+    int key = -1;
+    uint64_t step = 0;
+  } s_tab[4];
+  uint64_t fwd_step = 0;
   void split_gemm(moe_gemm_problem_t p, float* out_parts, uint64_t part_stride, int* nparts,
                   cudaStream_t st);
   const void* x_saved_ptr = nullptr;

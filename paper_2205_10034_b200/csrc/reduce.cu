@@ -113,6 +113,21 @@ __global__ void __launch_bounds__(RT) seg_colsum_kernel(uint32_t groups, const i
   }
 }
 
+// Few partials over many outputs (the split-fp32 weight gradients): one
+// float4 of outputs per thread, grid-stride, partials summed in index order.
+__global__ void __launch_bounds__(256) sum_few_parts_kernel(const float4* __restrict__ part,
+                                                            uint32_t nparts, uint64_t pstride4,
+                                                            uint64_t n4, float4* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    float4 s = __ldcg(part + i);
+    for (uint32_t q = 1; q < nparts; ++q) s = add4(s, __ldcg(part + (uint64_t)q * pstride4 + i));
+    out[i] = s;
+  }
+}
+
 }  // namespace
 
 void sum_parts(const float* part, uint32_t nparts, uint64_t part_stride, uint64_t rows,
@@ -121,7 +136,12 @@ void sum_parts(const float* part, uint32_t nparts, uint64_t part_stride, uint64_
   if (!n) return;
   const bool vec = cols % 4 == 0 && ldp % 4 == 0 && part_stride % 4 == 0 &&
                    (reinterpret_cast<uintptr_t>(part) & 15) == 0;
-  if (vec)
+  if (vec && nparts <= 8 && !transpose && ldp == cols && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+    const uint64_t n4 = n / 4;
+    const unsigned blocks = (unsigned)std::min<uint64_t>(ceil_div(n4, (uint64_t)256), (uint64_t)num_sms() * 16);
+    launch_pdl(sum_few_parts_kernel, blocks, 256, 0, st, reinterpret_cast<const float4*>(part),
+               nparts, part_stride / 4, n4, reinterpret_cast<float4*>(out));
+  } else if (vec)
     launch_pdl(sum_parts_kernel<true>, (unsigned)ceil_div(n, (uint64_t)128), RT, 0, st, part,
                nparts, part_stride, rows, cols, ldp, transpose ? 1 : 0, out);
   else

@@ -698,11 +698,12 @@ __global__ void colsum_kernel(const int32_t* __restrict__ gm, const int32_t* __r
   pdl_trigger();
   const int g = blockIdx.x;
   const int rows = gm[g];
-  const int r0 = blockIdx.y * 128;
+  constexpr int CH = 32;  // rows per block (partials reduced by seg_colsum)
+  const int r0 = blockIdx.y * CH;
   if (r0 >= rows) return;
   const int n = blockIdx.z * blockDim.x + threadIdx.x;
   if (n >= N) return;
-  const int r1 = min(rows, r0 + 128);
+  const int r1 = min(rows, r0 + CH);
   const T* base = X + ((uint64_t)ga[g] + r0) * N + n;
   float s = 0.f;
   for (int r = r0; r < r1; ++r, base += N) s += (float)*base;
@@ -972,8 +973,8 @@ void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, con
 }
 
 uint64_t colsum_ws_floats(uint32_t groups, uint32_t N, uint64_t max_rows) {
-  // the finest chunking of any colsum path (64 rows, colsum_bf16x8_kernel)
-  return (uint64_t)groups * std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)64)) * N;
+  // the finest chunking of any colsum path (32 rows, colsum_kernel)
+  return (uint64_t)groups * std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)32)) * N;
 }
 uint64_t colsum_ticket_ints(uint32_t groups, uint32_t N) {
   return (uint64_t)groups * ceil_div((uint64_t)N, (uint64_t)256);
@@ -995,7 +996,7 @@ void group_colsum(uint32_t groups, const int32_t* gm, const int32_t* ga, const i
   // several groups per output (or fp32): chunk partials into part_ws, then a
   // fixed-order segmented sum over (group, chunk) -- deterministic
   arg_check(part_ws != nullptr, "colsum.part_ws: workspace required");
-  const uint32_t chunk = dt == MOE_DTYPE_BF16 && N % 8 == 0 ? 64 : 128;
+  const uint32_t chunk = dt == MOE_DTYPE_BF16 && N % 8 == 0 ? 64 : 32;
   const uint32_t maxch = (uint32_t)std::max<uint64_t>(1, ceil_div(max_rows, (uint64_t)chunk));
   if (chunk == 64) {
     dim3 grid(groups, maxch, (unsigned)ceil_div(N / 8, 128));
