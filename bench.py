@@ -529,7 +529,7 @@ def main():
         kname, bound = ("tc_gemm_kernel (6 expert GEMMs/step: ffn1, ffn2, 2x dgrad, 2x wgrad)",
                         "tensor")
         psrc = pk["source"] + (", burst (timed region at max SM clock)" if burst else ", sustained")
-    elif ws == 1 and d % 128 == 0 and dff % 128 == 0 and os.environ.get("MOE_F32_GEMM") != "simt":
+    elif d % 128 == 0 and dff % 128 == 0 and os.environ.get("MOE_F32_GEMM") != "simt":
         # c1: fp32 expert GEMMs as split-bf16 tcgen05 GEMMs (f32split.cu): six
         # bf16 plane products per fp32 product, so the fp32 ceiling is 1/6 of bf16
         peak = (pk["bf16_tflops"] if burst else pk["bf16_tflops_sustained"]) / 6.0

@@ -6,7 +6,7 @@ NG=$(nvidia-smi -L | wc -l)
 nvidia-smi --query-gpu=name,clocks.max.sm --format=csv,noheader | head -1
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -2 gpurun_out/${TAG}_pytest_gpu.log
-timeout 400 python bench.py > gpurun_out/${TAG}_c2_n1.json 2> gpurun_out/${TAG}_c2_n1.err; echo "c2 n1 rc=$?"
+timeout 400 python bench.py --timeline gpurun_out/${TAG}_c2_n1_timeline.json > gpurun_out/${TAG}_c2_n1.json 2> gpurun_out/${TAG}_c2_n1.err; echo "c2 n1 rc=$?"
 timeout 400 python bench.py --impl reference > gpurun_out/${TAG}_reference_n1.json 2> gpurun_out/${TAG}_reference_n1.err; echo "ref rc=$?"
 for c in c1 c3 c4; do
   timeout 300 python bench.py --config $c --no-cpu > gpurun_out/${TAG}_${c}_n1.json 2> gpurun_out/${TAG}_${c}_n1.err; echo "$c n1 rc=$?"

@@ -86,11 +86,11 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   comm = d.nccl_comm;
   const double c = (double)k * d.capacity_factor * (double)T / (double)E;
   C = (uint64_t)std::ceil(c);
-  // fp32 layers run their expert GEMMs as split-bf16 tcgen05 GEMMs (one
-  // rank, widths the tcgen05 tiles take); MOE_F32_GEMM=simt keeps the FFMA path
+  // fp32 layers run their expert GEMMs as split-bf16 tcgen05 GEMMs (widths the
+  // tcgen05 tiles take); MOE_F32_GEMM=simt keeps the FFMA path
   {
     const char* env = std::getenv("MOE_F32_GEMM");
-    split32 = dt == MOE_DTYPE_F32 && P == 1 && dm % 128 == 0 && dff % 128 == 0 &&
+    split32 = dt == MOE_DTYPE_F32 && dm % 128 == 0 && dff % 128 == 0 &&
               !(env && std::string(env) == "simt");
   }
   pad = (dt == MOE_DTYPE_BF16 || split32) ? 64 : 1;
@@ -100,7 +100,8 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
       while (K / n > 512 || (K / 64) % n) ++n;
       return n;
     };
-    const uint64_t cs = round_up((uint64_t)std::ceil((double)k * d.capacity_factor * (double)T /
+    const uint64_t cs = (P > 1 && d.exchange == MOE_EXCHANGE_P2P ? P : 1) *
+                        round_up((uint64_t)std::ceil((double)k * d.capacity_factor * (double)T /
                                                      (double)E), 64);
     const uint64_t nmax =
         std::max({nchunks(dm), nchunks(dff), ceil_div(std::max<uint64_t>(cs, 1), (uint64_t)512)});
@@ -169,6 +170,8 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
   gmk = dalloc<int32_t>(owned, E);
   gak = dalloc<int32_t>(owned, E);
   gbk = dalloc<int32_t>(owned, E);
+  // rows per expert group: the P2P receive region holds every source's rows
+  gstride = p2p ? (uint64_t)P * Cs : Cs;
   if (split32) {
     const uint64_t kc = 512;  // K chunk: bounds the truncating tensor-core accumulation
     xr3 = dalloc_bytes(owned, 3 * rows * dm * 2);
@@ -178,8 +181,8 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
     w1_3 = dalloc_bytes(owned, 3 * (uint64_t)El * dff * dm * 2);
     w2_3 = dalloc_bytes(owned, 3 * (uint64_t)El * dff * dm * 2);
     const uint64_t np_m = std::max(ceil_div((uint64_t)dm, kc) * dff, ceil_div((uint64_t)dff, kc) * dm);
-    s_part = dalloc<float>(owned, std::max(np_m * rows, ceil_div(Cs, kc) * El * dff * dm));
-    s_cs = dalloc<float>(owned, colsum_ws_floats(ngroups, dff, Cs));
+    s_part = dalloc<float>(owned, std::max(np_m * rows, ceil_div(gstride, kc) * El * dff * dm));
+    s_cs = dalloc<float>(owned, colsum_ws_floats(ngroups, dff, gstride));
     const uint64_t nt = (uint64_t)E * 64;  // groups x K chunks (chunks <= 64)
     for (auto& t : s_tab) {
       t.m = dalloc<int32_t>(owned, nt);
@@ -325,7 +328,7 @@ void Layer::split_gemm(moe_gemm_problem_t p, float* out_parts, uint64_t part_str
     p.c_rows = n * rows;
     *nparts = (int)n;
   } else {
-    const uint32_t n = (uint32_t)ceil_div(Cs, (uint64_t)512);
+    const uint32_t n = (uint32_t)ceil_div(gstride, (uint64_t)512);
     const ChunkTables& t = tables(1, n, 512);
     arg_check(part_stride == (uint64_t)p.num_b * p.M * p.N, "split_gemm: RAGGED_K partial stride");
     p.groups = G * n;
@@ -438,7 +441,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     p.ldc = dff;
     split_gemm(p, s_part, rows * dff, &np, st);
     // A = gelu(h) goes straight to its bf16 planes (ffn2's and wgrad-w2's operand)
-    split_finish(1, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)Cs, dff, w.b1, nullptr,
+    split_finish(1, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)gstride, dff, w.b1, nullptr,
                  nullptr, static_cast<float*>(Gp), a3, rows * dff, st);
     mark("ffn1", st);
     p = expert_problem();
@@ -448,7 +451,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
     p.B = w2_3;
     p.ldc = dm;
     split_gemm(p, s_part, rows * dm, &np, st);
-    split_finish(0, s_part, np, rows * dm, ngroups, gm, ga, gb, (uint32_t)Cs, dm, w.b2, nullptr,
+    split_finish(0, s_part, np, rows * dm, ngroups, gm, ga, gb, (uint32_t)gstride, dm, w.b2, nullptr,
                  static_cast<float*>(Yl), nullptr, nullptr, 0, st);
   } else {
   {
@@ -600,9 +603,9 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
       p.groups = ngroups;
       p.a_rows = rows;
       p.num_b = El;
-      p.m = gmk;
-      p.a_row = gak;
-      p.b = gbk;
+      p.m = p2p ? gm : gmk;
+      p.a_row = p2p ? ga : gak;
+      p.b = p2p ? gb : gbk;
       p.M = w1 ? dff : dm;
       p.N = w1 ? dm : dff;
       p.A = w1 ? dh3 : dy3;
@@ -658,10 +661,10 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.B = w2_3;
     p.ldc = dff;
     split_gemm(p, s_part, rows * dff, &np, st);
-    split_finish(2, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)Cs, dff, nullptr,
+    split_finish(2, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)gstride, dff, nullptr,
                  static_cast<const float*>(Gp), static_cast<float*>(dH), nullptr, dh3, rows * dff,
                  st);
-    group_colsum(ngroups, gm, ga, gb, El, dff, dt, dH, g.db1, st, Cs, s_cs, nullptr);
+    group_colsum(ngroups, gm, ga, gb, El, dff, dt, dH, g.db1, st, gstride, s_cs, nullptr);
     mark("dgrad_ffn2", st);
     p = expert_problem();
     p.b_mn_major = 1;
@@ -671,7 +674,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.B = w1_3;
     p.ldc = dm;
     split_gemm(p, s_part, rows * dm, &np, st);
-    split_finish(0, s_part, np, rows * dm, ngroups, gm, ga, gb, (uint32_t)Cs, dm, nullptr, nullptr,
+    split_finish(0, s_part, np, rows * dm, ngroups, gm, ga, gb, (uint32_t)gstride, dm, nullptr, nullptr,
                  static_cast<float*>(dXl), nullptr, nullptr, 0, st);
   } else {
   {

@@ -86,6 +86,7 @@ struct Layer {
   // fp32 expert GEMMs on the bf16 tensor cores (f32split.cu): three bf16
   // planes per operand, K-chunk partials summed in fp32 by split_finish
   bool split32 = false;
+  uint64_t gstride = 0;  // rows per expert group (P2P: P * Cs, else Cs)
   void *xr3 = nullptr, *a3 = nullptr, *dy3 = nullptr, *dh3 = nullptr, *w1_3 = nullptr,
        *w2_3 = nullptr;
   float* s_part = nullptr;        // K-chunk partials
