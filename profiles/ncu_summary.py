@@ -38,6 +38,7 @@ ROLE = {
     "<256, 1, 1, 1, 0, 1, 2, 0>": "wgrad (fp32 dW)",
     "<256, 0, 1, 0, 4, 0, 2, 0>": "gate dgrad + gather dx",
     "<64, 1, 1, 1, 3, 1, 1, 0>": "gate wgrad (atomic)",
+    "<64, 1, 1, 1, 0, 1, 1, 0>": "gate wgrad (split-K partials)",
     "<64, 0, 0, 0, 0, 1, 1, 0>": "gate logits",
     "<256, 0, 0, 0, 0, 0, 2, 1>": "ffn2 + remote Y return (EP)",
     "<256, 0, 1, 0, 0, 0, 2, 1>": "dgrad ffn1 + remote dX return (EP)",
