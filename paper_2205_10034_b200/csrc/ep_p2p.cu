@@ -90,14 +90,15 @@ __device__ void grid_done_signal(const Win& w, uint32_t* ctr, int slot, uint64_t
 // survives and the host can read the code (moe_layer_comm_status) and recover
 // or abort.  Once *err is set every later wait returns at once (fail fast).
 __global__ void p2p_wait_kernel(const uint64_t* flags, uint32_t P, uint32_t me, int slot,
-                                uint64_t target, int32_t* err, uint64_t timeout_ns) {
+                                uint64_t target, int32_t* err, uint64_t timeout_ns,
+                                int fail_fast = 1) {
   const uint32_t p = threadIdx.x;
   if (p < P && p != me) {
     const uint64_t* f = flags + (uint64_t)slot * P + p;
     const uint64_t t0 = globaltimer();
     volatile int32_t* verr = err;
     while (ld_acquire_sys(f) < target) {
-      if (*verr != 0) break;
+      if (fail_fast && *verr != 0) break;
       if (timeout_ns && globaltimer() - t0 > timeout_ns) {
         atomicCAS(err, 0, 1000 + slot * 16 + (int)p);
         break;
@@ -454,8 +455,10 @@ void p2p_teardown(P2PWindow& w) {
     if (cudaDeviceSynchronize() == cudaSuccess &&
         cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess) {
       p2p_signal_kernel<<<1, 32, 0, st>>>(win_of(w), SLOT_BYE, 1);
+      // the BYE wait does not fail fast on an earlier error: a late peer
+      // still gets the full timeout to stop writing before the window goes
       p2p_wait_kernel<<<1, 32, 0, st>>>(reinterpret_cast<const uint64_t*>(w.base + w.off_flags),
-                                         w.P, w.me, SLOT_BYE, 1, w.err, w.timeout_ns);
+                                         w.P, w.me, SLOT_BYE, 1, w.err, w.timeout_ns, 0);
       cudaStreamSynchronize(st);
       cudaStreamDestroy(st);
     }

@@ -98,6 +98,38 @@ def _worker(rank, world, port, case, q):
             gb.close()
             q.put((rank, "ok"))
             return
+        if case == "timeout":
+            # a peer that never arrives: the waiting rank gives up after the
+            # peer timeout WITHOUT trapping, reports it through comm_status,
+            # keeps a usable CUDA context, and teardown still completes
+            import time
+            from paper_2205_10034_b200._lib import NcclError
+            cfg = MoEConfig(8, 1, 128, 256, 1.25, 256, torch.bfloat16)
+            lay = MoELayer(cfg, ep=ep)
+            lay.init_params(3)
+            x = lay.make_input(3)
+            if rank == 0:
+                lay.set_peer_timeout(1.0)
+                t0 = time.time()
+                lay.forward(x)
+                torch.cuda.synchronize()
+                waited = time.time() - t0
+                try:
+                    lay.comm_status()
+                    raise AssertionError("comm_status did not report the late peer")
+                except NcclError as e:
+                    assert "did not signal" in str(e), str(e)
+                assert 0.9 < waited < 60, waited
+                assert torch.ones(4, device="cuda").sum().item() == 4.0  # context alive
+            else:
+                time.sleep(4.0)
+                assert lay.comm_status() == 0
+            dist.barrier()
+            lay.close()
+            ep.close()
+            dist.destroy_process_group()
+            q.put((rank, "ok"))
+            return
         if isinstance(case, tuple) and case[0] == "stack":
             # config c4 as a block stack: gate gradients reduced by ONE fused
             # bucket all-reduce per step == each layer reducing its own
@@ -220,6 +252,10 @@ def test_gradient_buckets_allreduce():
 ])
 def test_ep_layer_matches_single_gpu(case):
     _run(case, world=min(torch.cuda.device_count(), 2))
+
+
+def test_late_peer_times_out_without_trapping():
+    _run("timeout", world=2)
 
 
 @pytest.mark.parametrize("exch", ["p2p", "nccl"])
