@@ -464,15 +464,18 @@ def main():
     barrier()  # ranks leave the clock sampler at different times: re-align first
     model.set_profiling(True)
     phase_tot = {}
+    # K steps back to back without a host sync (the host stays ahead of the
+    # GPU, so no phase carries a host-enqueue gap); the last step's per-phase
+    # events stand for every step
     for _ in range(args.steps):
         model.forward(x)
-        fwd_ph = model.phase_list()
-        for n, v in fwd_ph:
-            phase_tot["fwd." + n] = phase_tot.get("fwd." + n, 0.0) + v
         model.backward(dy, d_aux=0.01)
-        bwd_ph = model.phase_list()
-        for n, v in bwd_ph:
-            phase_tot["bwd." + n] = phase_tot.get("bwd." + n, 0.0) + v
+    fwd_ph = model.phase_list("fwd")
+    bwd_ph = model.phase_list("bwd")
+    for n, v in fwd_ph:
+        phase_tot["fwd." + n] = phase_tot.get("fwd." + n, 0.0) + v * args.steps
+    for n, v in bwd_ph:
+        phase_tot["bwd." + n] = phase_tot.get("bwd." + n, 0.0) + v * args.steps
     model.set_profiling(False)
     if args.timeline and rank == 0:
         # the last profiled step as the reference's trace-event JSON

@@ -360,6 +360,11 @@ moe_status_t moe_layer_host_sync(moe_layer_t layer, void* stream);
 moe_status_t moe_layer_set_profiling(moe_layer_t layer, int enabled);
 moe_status_t moe_layer_phase_times(moe_layer_t layer, const char** names, float* ms,
                                    uint32_t capacity, uint32_t* count);
+/* The same for the last forward (backward = 0) or the last backward (1): the
+ * two are recorded into separate events, so both can be read after one
+ * forward + backward without a synchronisation in between. */
+moe_status_t moe_layer_phase_times_of(moe_layer_t layer, int backward, const char** names,
+                                      float* ms, uint32_t capacity, uint32_t* count);
 
 /* Peer-wait limit of the NVLink exchange (default MOE_P2P_TIMEOUT_S or 600 s;
  * 0 = wait forever, like NCCL).  A peer that misses it does not kill the

@@ -244,6 +244,8 @@ SIGNATURES = {
     "moe_layer_comm_status": (_I, [_VP, C.POINTER(C.c_int32)]),
     "moe_layer_phase_times": (_I, [_VP, C.POINTER(C.c_char_p), C.POINTER(_F), _U32,
                                    C.POINTER(_U32)]),
+    "moe_layer_phase_times_of": (_I, [_VP, _I, C.POINTER(C.c_char_p), C.POINTER(_F), _U32,
+                                   C.POINTER(_U32)]),
     "moe_comm_unique_id": (_I, [_VP]),
     "moe_comm_create": (_I, [_VP, _U32, _U32, C.POINTER(_VP)]),
     "moe_comm_destroy": (_I, [_VP]),

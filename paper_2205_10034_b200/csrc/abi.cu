@@ -506,20 +506,35 @@ moe_status_t moe_layer_comm_status(moe_layer_t layer, int32_t* code) {
   });
 }
 
+static void phase_times_of(moe::Layer* L, int which, const char** names, float* ms,
+                           uint32_t capacity, uint32_t* count) {
+  uint32_t n = 0;
+  const auto& lg = L->plog[which];
+  if (L->profiling && lg.n > 0) {
+    MOE_CUDA(cudaEventSynchronize(lg.ev[lg.n]));
+    for (int i = 0; i < lg.n && n < capacity; ++i, ++n) {
+      if (names) names[n] = lg.name[i];
+      if (ms) MOE_CUDA(cudaEventElapsedTime(&ms[n], lg.ev[i], lg.ev[i + 1]));
+    }
+  }
+  *count = n;
+}
+
 moe_status_t moe_layer_phase_times(moe_layer_t layer, const char** names, float* ms,
                                    uint32_t capacity, uint32_t* count) {
   return guard([&] {
     moe::arg_check(layer != nullptr && count != nullptr, "phase_times: null argument");
     auto* L = reinterpret_cast<moe::Layer*>(layer);
-    uint32_t n = 0;
-    if (L->profiling && L->nphase > 0) {
-      MOE_CUDA(cudaEventSynchronize(L->ev[L->nphase]));
-      for (int i = 0; i < L->nphase && n < capacity; ++i, ++n) {
-        if (names) names[n] = L->phase_name[i];
-        if (ms) MOE_CUDA(cudaEventElapsedTime(&ms[n], L->ev[i], L->ev[i + 1]));
-      }
-    }
-    *count = n;
+    phase_times_of(L, L->last_log, names, ms, capacity, count);
+  });
+}
+
+moe_status_t moe_layer_phase_times_of(moe_layer_t layer, int backward, const char** names,
+                                      float* ms, uint32_t capacity, uint32_t* count) {
+  return guard([&] {
+    moe::arg_check(layer != nullptr && count != nullptr, "phase_times: null argument");
+    phase_times_of(reinterpret_cast<moe::Layer*>(layer), backward ? 1 : 0, names, ms, capacity,
+                   count);
   });
 }
 

@@ -240,12 +240,14 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
     MOE_CUDA(cudaMemcpy(split_a, sa.data(), nsplit * 4, cudaMemcpyHostToDevice));
     MOE_CUDA(cudaMemcpy(split_b, sb.data(), nsplit * 4, cudaMemcpyHostToDevice));
   }
-  for (int i = 0; i < kMaxPhases + 1; ++i) MOE_CUDA(cudaEventCreate(&ev[i]));
+  for (auto& lg : plog)
+    for (int i = 0; i < kMaxPhases + 1; ++i) MOE_CUDA(cudaEventCreate(&lg.ev[i]));
 }
 
 Layer::~Layer() {
   if (p2p) p2p_teardown(win);  // device sync + BYE handshake, then unmap / free
-  for (int i = 0; i < kMaxPhases + 1; ++i) cudaEventDestroy(ev[i]);
+  for (auto& lg : plog)
+    for (int i = 0; i < kMaxPhases + 1; ++i) cudaEventDestroy(lg.ev[i]);
   for (void* p : owned) cudaFree(p);
   if (x_stage) {
     for (int i = 0; i < 3; ++i) cudaStreamSynchronize(hp_stream[i]);
@@ -258,10 +260,11 @@ Layer::~Layer() {
 }
 
 void Layer::mark(const char* name, cudaStream_t st) {
-  if (!profiling || nphase >= kMaxPhases) return;
-  phase_name[nphase] = name;
-  MOE_CUDA(cudaEventRecord(ev[nphase + 1], st));
-  ++nphase;
+  PhaseLog& lg = plog[cur_log];
+  if (!profiling || lg.n >= kMaxPhases) return;
+  lg.name[lg.n] = name;
+  MOE_CUDA(cudaEventRecord(lg.ev[lg.n + 1], st));
+  ++lg.n;
 }
 
 void Layer::a2a(const void* send, void* recv, uint64_t bytes_per_peer, cudaStream_t st) {
@@ -362,9 +365,10 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   arg_check((x != nullptr && y != nullptr) || T == 0, "forward.x/y: must be non-null");
   arg_check(w.w1 && w.w2 && w.b1 && w.b2, "forward.params: expert weights must be non-null");
   arg_check(override_logits || w.wg, "forward.params.wg: gate weight required");
-  nphase = 0;
+  cur_log = last_log = 0;
+  plog[0].n = 0;
   x_saved_ptr = x;
-  if (profiling) MOE_CUDA(cudaEventRecord(ev[0], st));
+  if (profiling) MOE_CUDA(cudaEventRecord(plog[0].ev[0], st));
   const uint64_t ph = ++phase;
   ++fwd_step;  // new group tables this step: the split-fp32 chunk tables go stale
   if (p2p) p2p_wait(win, SLOT_PHASE, ph - 1, st);  // peers done reading our previous writes
@@ -524,8 +528,9 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   arg_check((dy != nullptr && dx != nullptr) || T == 0, "backward.dy/dx: must be non-null");
   arg_check(g.dw1 && g.db1 && g.dw2 && g.db2 && g.dwg, "backward.grads: must be non-null");
   arg_check(w.wg != nullptr, "backward.params.wg: gate weight required");
-  nphase = 0;
-  if (profiling) MOE_CUDA(cudaEventRecord(ev[0], st));
+  cur_log = last_log = 1;
+  plog[1].n = 0;
+  if (profiling) MOE_CUDA(cudaEventRecord(plog[1].ev[0], st));
   const uint64_t ph = ++phase;
   // K6^T: dgate and the gate-scaled dY into the send layout (+ zero pad rows),
   // or straight into the owning ranks' receive buffers (P2P)

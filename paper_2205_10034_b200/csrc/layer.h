@@ -112,9 +112,15 @@ struct Layer {
   bool has_forward = false;
   // profiling
   bool profiling = false;
-  int nphase = 0;
-  const char* phase_name[kMaxPhases] = {};
-  cudaEvent_t ev[kMaxPhases + 1] = {};
+  // per-phase events of the last forward (0) and the last backward (1): kept
+  // apart so a caller can read both after one synchronisation
+  struct PhaseLog {
+    int n = 0;
+    const char* name[kMaxPhases] = {};
+    cudaEvent_t ev[kMaxPhases + 1] = {};
+  } plog[2];
+  int cur_log = 0;   // the call being recorded
+  int last_log = 0;  // the most recent call
 };
 
 void comm_unique_id(uint8_t id[128]);

@@ -276,12 +276,17 @@ class MoELayer:
     def set_profiling(self, on: bool) -> None:
         call("moe_layer_set_profiling", self._h, 1 if on else 0)
 
-    def phase_list(self) -> List[Tuple[str, float]]:
-        """(phase, ms) of the last forward/backward in launch order (profiling on)."""
+    def phase_list(self, which: Optional[str] = None) -> List[Tuple[str, float]]:
+        """(phase, ms) in launch order (profiling on) of the last call, or of
+        the last forward / backward (which = "fwd" / "bwd")."""
         names = (C.c_char_p * 64)()
         ms = (C.c_float * 64)()
         n = C.c_uint32(0)
-        call("moe_layer_phase_times", self._h, names, ms, 64, C.byref(n))
+        if which is None:
+            call("moe_layer_phase_times", self._h, names, ms, 64, C.byref(n))
+        else:
+            call("moe_layer_phase_times_of", self._h, 1 if which == "bwd" else 0, names, ms, 64,
+                 C.byref(n))
         return [(names[i].decode(), float(ms[i])) for i in range(n.value)]
 
     def phase_times(self) -> Dict[str, float]:

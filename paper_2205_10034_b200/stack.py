@@ -76,11 +76,11 @@ class MoEStack:
         for layer in self.layers:
             layer.set_profiling(on)
 
-    def phase_list(self) -> List[Tuple[str, float]]:
-        """Phases of the last call of every layer (layer-major)."""
+    def phase_list(self, which: Optional[str] = None) -> List[Tuple[str, float]]:
+        """Phases of the last call (or forward / backward) of every layer."""
         out = []
         for layer in self.layers:
-            out += layer.phase_list()
+            out += layer.phase_list(which)
         return out
 
     def phase_times(self) -> Dict[str, float]:
