@@ -33,6 +33,9 @@ namespace moe {
 
 namespace tc {
 
+#ifndef MOE_COOP_GATHER
+#define MOE_COOP_GATHER 1
+#endif
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int THREADS = 384;
@@ -582,10 +585,34 @@ __global__ void __launch_bounds__(THREADS, 1)
       };
       if (EPI == MOE_EPI_GATHER_ADD) {
         static_assert(EPI != MOE_EPI_GATHER_ADD || (BN / 2) / C_::CW <= 4, "gather chunks");
+        if (MOE_COOP_GATHER && col_base + nch * CW <= args.N) {
+          // lanes cooperate per row: a warp instruction copies 2 (4) whole
+          // gathered row pieces of 256 (128) contiguous bytes instead of 32
+          // rows' 16-byte pieces -- coalesced reads of the scattered rows.
+          // One cp.async group for the tile (+3 empty ones: same waits below)
+          const int ppr = nch * 4, rpi = 32 / ppr;  // 16-byte pieces per row, rows per step
+          const int q = lane % ppr, cq = q >> 2, jq = q & 3;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          if (cc < nch) gather_prefetch(cc);
-          else cp_async_commit();
+          for (int i = 0; i < 2; ++i) {
+            if (i >= args.gk) break;
+            for (int r0 = 0; r0 < 32; r0 += rpi) {
+              const int r = r0 + lane / ppr;
+              const int gi = __shfl_sync(0xffffffffu, gidx[i], r);
+              if (gi >= 0) {
+                const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(args.gsrc) +
+                                           (long long)gi * args.N + col_base + q * 8;
+                cp_async16(smem_u32(auxb + (i * 4 + cq) * STG) + sw64(r, jq), src);
+              }
+            }
+          }
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) cp_async_commit();
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            if (cc < nch) gather_prefetch(cc);
+            else cp_async_commit();
+          }
         }
       }
       const bool has_k = num_kblocks(g) > 0;
@@ -687,6 +714,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           else if (c == 1) cp_async_wait<2>();
           else if (c == 2) cp_async_wait<1>();
           else cp_async_wait<0>();
+          if (MOE_COOP_GATHER) __syncwarp();  // other lanes' copies of this lane's row
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             if (gidx[i] < 0) continue;
