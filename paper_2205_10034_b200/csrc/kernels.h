@@ -66,7 +66,7 @@ void route_backward(uint64_t T, uint32_t E, uint32_t k, const float* logits, con
                     const float* dgate, float d_aux, float* dlogits_f32, void* dlogits_lp,
                     moe_dtype_t lp_dtype, uint32_t ld, float* dbg, float* dbg_ws,
                     cudaStream_t st);
-inline uint64_t route_dbg_ws_floats(uint64_t T, uint32_t E) { return ((T + 255) / 256) * E; }
+inline uint64_t route_dbg_ws_floats(uint64_t T, uint32_t E) { return ((T + 63) / 64) * E; }
 
 // K3: dispatch tokens into the slot buffer [E][C][d] (send layout: rank-major,
 // then local expert, then position).  slot[t*k+i] = e*C+pos or -1.
