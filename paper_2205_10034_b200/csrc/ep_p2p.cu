@@ -21,8 +21,10 @@
 // 0 = never) by recording an error code instead of trapping; teardown is a
 // flag handshake so no peer store can land in a freed window.
 //
-// Receive order follows alltoall_flat (collectives.cpp:10-21): sources in rank
-// order inside every expert region.
+// Receive order: alltoall_flat's source rank order (collectives.cpp:10-21)
+// rotated to start at the receiver (its own rows first, then r+1, ..., r-1),
+// so the receiver's expert GEMM can start on its local rows before any peer
+// row lands.
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -127,10 +129,21 @@ __global__ void p2p_counts_kernel(Win w, uint32_t* ctr, const int32_t* __restric
 }
 
 // offset of source `me`'s rows inside expert e's region on its owner
-__device__ __forceinline__ int src_offset(const int32_t* cnt, uint32_t E, uint32_t me, int e) {
+// Receive order inside a region: the receiver's own rows first, then the
+// other sources in rank order from there (receiver r: r, r+1, ..., r-1), so a
+// receiver can run its local rows before any peer row has landed.
+// Offset of source `src`'s rows of expert e in receiver `recv`'s region:
+__device__ __forceinline__ int rot_offset(const int32_t* cnt, uint32_t E, uint32_t P,
+                                          uint32_t recv, uint32_t src, int e) {
   int off = 0;
-  for (uint32_t s = 0; s < me; ++s) off += cnt[(uint64_t)s * E + e];
+  const uint32_t n = (src + P - recv) % P;
+  for (uint32_t i = 0; i < n; ++i) off += cnt[(uint64_t)((recv + i) % P) * E + e];
   return off;
+}
+// offset of this rank's rows in the region of expert e (owner e / El)
+__device__ __forceinline__ int src_offset(const int32_t* cnt, uint32_t E, uint32_t P, uint32_t El,
+                                          uint32_t me, int e) {
+  return rot_offset(cnt, E, P, (uint32_t)e / El, me, e);
 }
 
 constexpr int MAXE = 256;
@@ -146,7 +159,7 @@ __global__ void __launch_bounds__(256) p2p_dispatch_kernel(
     int32_t* __restrict__ slot, uint64_t epoch) {
   __shared__ int off_s[MAXE];
   const int32_t* cnt = cnt_of(w);
-  for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) off_s[e] = src_offset(cnt, w.E, w.me, e);
+  for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) off_s[e] = src_offset(cnt, w.E, w.P, w.El, w.me, e);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nv = (int)(w.row_bytes / 16);
@@ -251,7 +264,7 @@ __global__ void __launch_bounds__(256) p2p_combine_bwd_kernel(
     float* __restrict__ dgate, uint64_t epoch) {
   __shared__ int off_s[MAXE];
   const int32_t* cnt = cnt_of(w);
-  for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) off_s[e] = src_offset(cnt, w.E, w.me, e);
+  for (uint32_t e = threadIdx.x; e < w.E; e += blockDim.x) off_s[e] = src_offset(cnt, w.E, w.P, w.El, w.me, e);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const T* Yh = reinterpret_cast<const T*>(w.peers[w.me] + off_yh);
@@ -297,8 +310,7 @@ __global__ void __launch_bounds__(256) p2p_push_kernel(Win w, uint64_t home_off,
   const int j = blockIdx.x / w.P, s = blockIdx.x % w.P;
   const int e = (int)(w.me * w.El) + j;
   const int32_t* cnt = cnt_of(w);
-  int off = 0;
-  for (int q = 0; q < s; ++q) off += cnt[(uint64_t)q * w.E + e];
+  const int off = rot_offset(cnt, w.E, w.P, w.me, (uint32_t)s, e);
   const int n = cnt[(uint64_t)s * w.E + e];
   const int r0 = blockIdx.y * 64;
   const uint64_t nv = w.row_bytes / 16;

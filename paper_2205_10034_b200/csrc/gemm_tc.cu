@@ -516,12 +516,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int g = geo.g;
       const int row0 = geo.row0, nch = geo.nch, nvalid = geo.nvalid, bidx = geo.bidx, tcol = geo.tcol;
       const long long orow0 = geo.orow0;
-      // REMOTE: lane s holds the exclusive row offset of source s inside this
-      // expert's contiguous receive region
+      // REMOTE: lane i holds the exclusive row offset, inside this expert's
+      // contiguous receive region, of source (me + i) % P -- the receiver
+      // keeps its own rows first (rotated source order, ep_p2p.cu)
       int rexcl = 0, rexp = 0;
       if (REMOTE) {
         rexp = ro.me * ro.El + bidx;
-        const int cv = lane < ro.P ? ro.cnt[lane * ro.E + rexp] : 0;
+        const int cv = lane < ro.P ? ro.cnt[((ro.me + lane) % ro.P) * ro.E + rexp] : 0;
         int incl = cv;
 #pragma unroll
         for (int o = 1; o < 8; o <<= 1) {
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         rexcl = incl - cv;
       }
-      // source rank of group row r (warp-collective: every lane must call it)
+      // rotated position of the source of group row r (warp-collective)
       auto src_of = [&](int r) {
         int sidx = 0;
 #pragma unroll
@@ -744,12 +745,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (REMOTE) {
           // return all-to-all fused into the epilogue: rows go straight to the
           // source rank's buffer over NVLink
-          const int sl = src_of(row0 + lane);                    // this lane's row
-          const int offl = __shfl_sync(0xffffffffu, rexcl, sl);
-          const int s0 = __shfl_sync(0xffffffffu, sl, 0);
-          const int s1 = __shfl_sync(0xffffffffu, sl, max(nvalid - 1, 0));
-          const int off0 = __shfl_sync(0xffffffffu, rexcl, s0);
-          if (full_tile && s0 == s1) {
+          const int pl = src_of(row0 + lane);                    // this lane's row
+          const int sl = (ro.me + pl) % ro.P;
+          const int offl = __shfl_sync(0xffffffffu, rexcl, pl);
+          const int p0 = __shfl_sync(0xffffffffu, pl, 0);
+          const int p1 = __shfl_sync(0xffffffffu, pl, max(nvalid - 1, 0));
+          const int off0 = __shfl_sync(0xffffffffu, rexcl, p0);
+          const int s0 = (ro.me + p0) % ro.P;
+          if (full_tile && p0 == p1) {
             if (lane == 0) {
               if (C_::NBUF == 2) bulk_wait_read1();
               else bulk_wait_read0();
