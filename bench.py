@@ -579,6 +579,28 @@ def main():
             per.append({"gemm": name, "ms": ms_k, "tflops": tf, "frac": tf / peak,
                         "hbm_GBps": gbs, "hbm_frac": gbs / pk["hbm_gbs"]})
     roof["per_gemm"] = per
+    if dtype == torch.bfloat16 and rank == 0:
+        # library reference: cuBLAS on the dense equivalent of each expert GEMM
+        # shape (all kept rows as one matrix, bf16 in, fp32 accumulate, bf16
+        # out, no epilogue) on the same GPU -- what a plain GEMM reaches here
+        R_ = int(rows_local) // 128 * 128
+        shapes = {"ffn1 (R x d -> d_ff)": (R_, d, dff), "ffn2 (R x d_ff -> d)": (R_, dff, d)}
+        cub = {}
+        for nm, (mm, kk, nn) in shapes.items():
+            a_ = torch.randn(mm, kk, device=dev, dtype=torch.bfloat16)
+            b_ = torch.randn(kk, nn, device=dev, dtype=torch.bfloat16)
+            for _ in range(3):
+                torch.matmul(a_, b_)
+            e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0_.record()
+            for _ in range(10):
+                torch.matmul(a_, b_)
+            e1_.record()
+            torch.cuda.synchronize()
+            t_ = e0_.elapsed_time(e1_) / 10
+            cub[nm] = {"ms": t_, "tflops": 2.0 * mm * kk * nn / (t_ / 1e3) / 1e12}
+            del a_, b_
+        roof["cublas_dense_equivalent"] = cub
 
     # ---- HBM roofline of the memory-bound kernels (gating, dispatch, combine
     # and their backward): algorithmic bytes = each operand read once + each
