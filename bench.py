@@ -698,7 +698,8 @@ def main():
         xbytes = L * kept_local * row_bytes * (ws - 1) / ws  # summed over the stack's layers
         ph = {n: v / args.steps for n, v in phase_tot.items()}
         if args.exchange == "p2p":
-            ex = {"dispatch": ph.get("fwd.dispatch_p2p", 0) + ph.get("fwd.a2a_dispatch", 0),
+            ex = {"dispatch": ph.get("fwd.a2a_counts", 0) + ph.get("fwd.dispatch_p2p", 0) +
+                  ph.get("fwd.a2a_dispatch", 0),
                   "combine": ph.get("fwd.a2a_combine", 0),
                   "dy": ph.get("bwd.combine_bwd", 0) + ph.get("bwd.a2a_dy", 0),
                   "dx": ph.get("bwd.a2a_dx", 0)}

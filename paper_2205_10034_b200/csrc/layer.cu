@@ -412,6 +412,7 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   if (p2p) {
     p2p_counts(win, dkept(), ph, st);
     p2p_wait(win, SLOT_CNT, ph, st);
+    mark("a2a_counts", st);  // count all-gather + waiting for the slowest peer's routing
     p2p_dispatch(win, T, dm, k, C, dt, x, dexp(), position, slot, ph, st);
     mark("dispatch_p2p", st);
     p2p_wait(win, SLOT_DISPATCH, ph, st);
