@@ -87,8 +87,13 @@ __device__ __forceinline__ void load_slab(const float* __restrict__ logits, uint
   }
 }
 
-// exp(x) as one FMUL + MUFU.EX2 (max relative error ~2^-21, against
-// libdevice expf's ~10 instructions); exp(-inf) = 0, NaN stays NaN.
+// exp(x) as one FMUL + MUFU.EX2 (against libdevice expf's ~10 instructions);
+// exp(-inf) = 0, NaN stays NaN.  Relative error: ex2.approx's ~2^-22 plus the
+// rounding of x * log2(e), ~|x| * log2(e) * 2^-24 (about 1e-6 at x = -20,
+// 5e-6 at x = -80), and .ftz flushes results below 2^-126 to zero -- only
+// the softmax normaliser and the aux-loss column sums use it, where those
+// terms are negligible tails.  The top-2 gates (the compared outputs) use the
+// precise expf of l2 - l1 and do not depend on the normaliser.
 __device__ __forceinline__ float exp_f(float x) { return ex2_approx(x * 1.44269504088896341f); }
 
 // Phase A: thread per token (the block is one 256-token chunk): top-k on the
