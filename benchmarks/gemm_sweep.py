@@ -37,6 +37,10 @@ def timed(fn, reps):
     return ts[len(ts) // 2]
 
 
+SHARED_B = False
+B_MOD = 0
+
+
 def ragged_m(G, rows, N, K, epi=0, b_mn=False, out_f32=False, colsum=True):
     A = torch.randn(G * rows, K, device=dev).to(torch.bfloat16)
     B = (torch.randn(G, K, N, device=dev) if b_mn else torch.randn(G, N, K, device=dev)).to(torch.bfloat16)
@@ -45,7 +49,7 @@ def ragged_m(G, rows, N, K, epi=0, b_mn=False, out_f32=False, colsum=True):
     C2 = torch.empty_like(Cm)
     aux = torch.randn(G * rows, N, device=dev).to(cdt)
     bias = torch.randn(G, N, device=dev)
-    m, ar, b = i32([rows] * G), i32([g * rows for g in range(G)]), i32(list(range(G)))
+    m, ar, b = i32([rows] * G), i32([g * rows for g in range(G)]), i32([0] * G if SHARED_B else [g % B_MOD if B_MOD else g for g in range(G)])
     cs = torch.zeros(G, N, device=dev)
     p = GemmProblem()
     p.kind, p.epilogue = _lib.MOE_GEMM_RAGGED_M, epi
@@ -89,7 +93,14 @@ def main():
     ap.add_argument("--groups", type=int, default=64)
     ap.add_argument("--only", default="", help="comma-separated substrings of variant names")
     ap.add_argument("--json", action="store_true")
+    ap.add_argument("--cublas", action="store_true",
+                    help="also time torch.matmul (cuBLAS) on the dense equivalents")
+    ap.add_argument("--shared-b", action="store_true", help="every group uses weight 0 (L2-resident)")
+    ap.add_argument("--b-mod", type=int, default=0, help="group g uses weight g %% B_MOD")
     a = ap.parse_args()
+    global SHARED_B, B_MOD
+    SHARED_B = a.shared_b
+    B_MOD = a.b_mod
     G, R, d, f = a.groups, a.rows, 1024, 4096
     variants = [
         ("ffn1 shape  K-major  bf16 STORE", lambda: ragged_m(G, R, f, d)),
@@ -114,6 +125,15 @@ def main():
         else:
             print(f"{name}  {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.1f} TFLOP/s", flush=True)
         del keep
+    if a.cublas:
+        T = G * R
+        for name, (M, N, K) in (("cuBLAS ffn1 dense", (T, f, d)), ("cuBLAS ffn2 dense", (T, d, f))):
+            X = torch.randn(M, K, device=dev).to(torch.bfloat16)
+            W = torch.randn(N, K, device=dev).to(torch.bfloat16)
+            Y = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
+            ms = timed(lambda: torch.matmul(X, W.t(), out=Y), a.reps)
+            print(f"{name:32s}  {ms * 1e3:8.1f} us  {2.0 * M * N * K / ms / 1e9:7.1f} TFLOP/s", flush=True)
+            del X, W, Y
 
 
 if __name__ == "__main__":

@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+S="ffn1 shape  K-major  bf16 STORE,ffn2,GELU,dgrad2 shp  B MN     bf16 DGELU,dgrad1"
+for r in 1 2; do for v in base pfb1 pfb2; do
+  echo "== $v 64x1024 ($r)"; MOE_B200_LIB=exp/$v/libmoe_b200.so python benchmarks/gemm_sweep.py --only "$S" --groups 64 --rows 1024
+done; done
+for v in base pfb1 pfb2; do echo "== $v 64x1030"; MOE_B200_LIB=exp/$v/libmoe_b200.so python benchmarks/gemm_sweep.py --only "ffn1 shape  K-major  bf16 STORE,ffn2" --groups 64 --rows 1030; done
+bash benchmarks/ab_bench.sh c2 2 base pfb1 pfb2

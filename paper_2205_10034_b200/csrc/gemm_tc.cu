@@ -21,6 +21,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -218,11 +219,26 @@ template <int BN, bool A_MN, bool B_MN, int KIND, int EPI, bool CF32, int CG, bo
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2,
-                   const __grid_constant__ CUtensorMap tmAux, const Args args,
+                   const __grid_constant__ CUtensorMap tmAux,
+                   const __grid_constant__ CUtensorMap tmAh, const Args args,
                    const __grid_constant__ RemoteOut ro) {
   using C_ = Cfg<BN, EPI, CF32, CG, KIND>;
   constexpr int TM = BM * CG;  // tile rows per work item (the CTA pair)
-  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0;  // 0 = leader
+  // Pair mode (cluster of 2): one CTA pair per cluster.  Multicast mode
+  // (cluster of 4, launched with a preferred cluster size of 4 where the
+  // tile grid allows): two pairs per cluster work on the two column blocks
+  // of one row block (consecutive work items), and each CTA loads half of
+  // the A rows it shares with its counterpart in the other pair and
+  // multicasts them to both -- a quarter less operand traffic through the
+  // L2, which bounds these GEMMs.  Clusters the GPU could only place as
+  // pairs run pair mode.
+  const uint32_t crank_c = CG == 2 ? cluster_ctarank() : 0;
+  const bool mc = CG == 2 && cluster_nctarank() == 4;
+  const uint32_t crank = crank_c & 1;      // rank inside the pair (0 = leader)
+  const uint32_t lead = crank_c & ~1u;     // the pair leader's cluster rank
+  const uint32_t ahalf = crank_c >> 1;     // multicast mode: the A half this CTA loads
+  const uint16_t pmask = (uint16_t)(3u << lead);
+  const uint16_t amask = (uint16_t)((1u << crank_c) | (1u << (crank_c ^ 2u)));
   const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int nunits = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   constexpr int CW = C_::CW;
@@ -255,7 +271,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 9 && lane == 0) {
     for (int s = 0; s < C_::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], mc ? 2 : 1);  // multicast: both pairs' MMAs read the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -301,6 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
   if (CG == 2) cluster_sync_all();  // peer barriers initialised before any TMA signals them
+  if (mc && (unit & 1) != (int)ahalf) __trap();  // clusters are aligned blockIdx quads
   tc_fence_after();
   const uint32_t tmem_base = *tmem_hold;
 
@@ -360,15 +377,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         decode(w, g, mb, nb);
         auto load = [&](void* dst, const CUtensorMap* m, int s, int c0, int c1) {
           if (CG == 2)
-            tma_load_2d_2sm(dst, m, mapa_shared(full0 + s * 8, 0), c0, c1);
+            tma_load_2d_2sm(dst, m, mapa_shared(full0 + s * 8, lead), c0, c1);
           else
             tma_load_2d(dst, m, &full[s], c0, c1);
+        };
+        // multicast half of the shared A rows (both pairs' CTAs of this rank)
+        auto load_mc = [&](void* dst, const CUtensorMap* m, int s, int c0, int c1) {
+          tma_load_2d_2sm_mc(dst, m, mapa_shared(full0 + s * 8, lead), amask, c0, c1);
         };
         auto arm = [&](int s) {
           if (crank == 0) mbar_arrive_expect_tx(&full[s], C_::STAGE_BYTES * CG);
         };
         if (KIND == 0) {
-          const int arow = args.ga[g] + mb * TM + (int)crank * (is_tail(g, mb) ? 64 : BM);
+          const bool tail = is_tail(g, mb);
+          const int arow = args.ga[g] + mb * TM + (int)crank * (tail ? 64 : BM);
           const int brow = args.gb[g] * (B_MN ? args.K : args.N);
           const int bcol = nb * BN + (int)crank * BH;
           const int nk = args.k_len / BK, kb0 = (args.gkb ? args.gkb[g] : args.k_begin) / BK;
@@ -383,7 +405,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint8_t* sA = smem + s * C_::STAGE_BYTES;
             uint8_t* sB = sA + C_::A_BYTES;
             arm(s);
-            load(sA, &tmA, s, kb * BK, arow + pa);  // A K-major box {64,128}
+            if (mc && !tail)  // this CTA's half: box {64, 64}, to both pairs
+              load_mc(sA + ahalf * 8192, &tmAh, s, kb * BK, arow + pa + (int)ahalf * 64);
+            else
+              load(sA, &tmA, s, kb * BK, arow + pa);  // A K-major box {64,128}
             if (!B_MN) {
               load(sB, &tmB, s, kb * BK, brow + bcol + pb);
             } else {
@@ -408,9 +433,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 uint8_t* sB = sA + C_::A_BYTES;
                 arm(s);
                 const int row = r0 + kb * BK;
+                if (mc) {
+                  load_mc(sA + ahalf * 8192, &tmA, s, acol + (int)ahalf * 64, row + pa);
+                } else {
 #pragma unroll
-                for (int j = 0; j < BM / 64; ++j)
-                  load(sA + j * 8192, &tmA, s, acol + j * 64, row + pa);
+                  for (int j = 0; j < BM / 64; ++j)
+                    load(sA + j * 8192, &tmA, s, acol + j * 64, row + pa);
+                }
 #pragma unroll
                 for (int j = 0; j < BH / 64; ++j)
                   load(sB + j * 8192, &tmB, s, bcol + j * 64, row + pb);
@@ -459,13 +488,13 @@ __global__ void __launch_bounds__(THREADS, 1)
               if (CG == 2) tc_mma_bf16_2sm(d_tmem, da0 + kk * ADV_A, db0 + kk * ADV_B, idesc, accum);
               else tc_mma_bf16(d_tmem, da0 + kk * ADV_A, db0 + kk * ADV_B, idesc, accum);
             }
-            if (CG == 2) tc_commit_2sm_mc(&empty[s], 0x3);
+            if (CG == 2) tc_commit_2sm_mc(&empty[s], mc ? (uint16_t)0xF : pmask);
             else tc_commit(&empty[s]);
           }
           if (kWarpIssue) __syncwarp();
         }
         if (!kWarpIssue || elect_one()) {
-          if (CG == 2) tc_commit_2sm_mc(&tfull[acc], 0x3);
+          if (CG == 2) tc_commit_2sm_mc(&tfull[acc], pmask);
           else tc_commit(&tfull[acc]);
         }
         if (kWarpIssue) __syncwarp();
@@ -824,7 +853,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(tempty0 + acc * 8, 0));
+        if (CG == 2) mbar_arrive_cluster_relaxed(mapa_shared(tempty0 + acc * 8, lead));
         else mbar_arrive(&tempty[acc]);
       }
     }
@@ -901,7 +930,7 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
     MOE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM));
     configured.fetch_or(bit, std::memory_order_acq_rel);
   }
-  CUtensorMap ta, tb, tcm, tc2, tax;
+  CUtensorMap ta, tb, tcm, tc2, tax, tah;
   const bool split = p.split_terms == 6;
   // split-fp32: the maps span the three stacked planes
   const uint64_t np = split ? 3 : 1;
@@ -910,6 +939,7 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
     const uint64_t lda = p.lda ? p.lda : p.K;
     a_plane = p.a_rows;
     ta = make_map(p.A, p.K, np * p.a_rows, lda, 64, BM);
+    tah = CG == 2 ? make_map(p.A, p.K, np * p.a_rows, lda, 64, 64) : ta;  // multicast halves
     if (!B_MN) {
       const uint64_t ldb = p.ldb ? p.ldb : p.K;
       const uint64_t rows = p.b_rows ? p.b_rows : (uint64_t)p.num_b * p.N;
@@ -927,6 +957,7 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
     a_plane = p.a_rows;
     b_plane = p.b_rows ? p.b_rows : p.a_rows;
     ta = make_map(p.A, p.M, np * p.a_rows, lda, 64, 64);
+    tah = ta;
     tb = make_map(p.B, p.N, np * b_plane, ldb, 64, 64);
   }
   const uint64_t c_rows = p.c_rows ? p.c_rows : (KIND == 0 ? p.a_rows : (uint64_t)p.num_b * p.M);
@@ -989,29 +1020,58 @@ static void launch(const moe_gemm_problem_t& p, cudaStream_t st,
   const int budget = gemm_cta_budget();
   const int grid = budget > 0 ? std::min(budget, num_sms()) : num_sms();
   if (CG == 1) {
-    launch_pdl(kern, grid, THREADS, C_::SMEM, st, ta, tb, tcm, tc2, tax, a, ro);
+    launch_pdl(kern, grid, THREADS, C_::SMEM, st, ta, tb, tcm, tc2, tax, tah, a, ro);
   } else {
     cudaLaunchConfig_t cfg = {};
+    // multicast mode needs an even number of column blocks (the two pairs of a
+    // cluster take consecutive ones) and whole quads of CTAs
+    const int nblk_n = (int)((p.N + BN - 1) / BN);
+    // (A/B on one B200, 64 experts: ffn2 / dgrad-ffn1 -2 to -3%, c2 step -0.7
+    // to -1%, c3 -0.3 to -1.4%, the dense equivalent -3%; the GeLU / GeLU'
+    // epilogue GEMMs, the fp32-output ones (c1 +1%) and the weight gradients
+    // are not operand-bound enough to gain: pair mode for them)
+    const bool mc = !REMOTE && gemm_multicast_enabled() && nblk_n % 2 == 0 &&
+                    (grid & 3) == 0 && KIND == 0 && EPI == MOE_EPI_STORE && !CF32;
     cfg.gridDim = dim3((unsigned)std::max(2, grid & ~1));
     cfg.blockDim = dim3(THREADS);
     cfg.dynamicSmemBytes = C_::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[3];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (mc) {
+      attr[na].id = cudaLaunchAttributePreferredClusterDimension;
+      attr[na].val.preferredClusterDim.x = 4;
+      attr[na].val.preferredClusterDim.y = 1;
+      attr[na].val.preferredClusterDim.z = 1;
+      ++na;
+    }
+    if (pdl_enabled()) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    MOE_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tc2, tax, a, ro));
+    cfg.numAttrs = na;
+    MOE_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tc2, tax, tah, a, ro));
   }
   MOE_LAUNCH_CHECK("tc_gemm_kernel");
   count_launch();
 }
 
 }  // namespace tc
+
+bool gemm_multicast_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MOE_GEMM_MC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 int& gemm_cta_budget() {
   thread_local int budget = 0;

@@ -31,6 +31,8 @@ struct RemoteRows {
 // thread may occupy (0: all SMs).  Used to run two GEMMs side by side on
 // disjoint SM sets; set with the scoped GemmCtaBudget.
 int& gemm_cta_budget();
+// MOE_GEMM_MC=0 disables the 2-pair multicast clusters of the expert GEMMs (A/B switch)
+bool gemm_multicast_enabled();
 struct GemmCtaBudget {
   int saved;
   explicit GemmCtaBudget(int n) : saved(gemm_cta_budget()) { gemm_cta_budget() = n; }
