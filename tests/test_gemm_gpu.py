@@ -340,3 +340,55 @@ def test_split_f32_ragged_k():
         ref = A[g * rows:(g + 1) * rows].double().t() @ B[g * rows:(g + 1) * rows].double()
         err = (C[g].double() - ref).abs().max() / ref.abs().max()
         assert err < 2e-6, (g, err.item())
+
+
+_MC_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2205_10034_b200 import _lib, grouped_gemm
+from paper_2205_10034_b200._lib import GemmProblem
+dev = torch.device("cuda")
+torch.manual_seed(1)
+groups, Cs, N, K = (1030, 0, 37, 700, 256, 129), 1088, 1024, 512
+G = len(groups)
+A = (torch.rand(G * Cs, K, device=dev) * 2 - 1).to(torch.bfloat16)
+B = ((torch.rand(G, N, K, device=dev) * 2 - 1) / K ** 0.5).to(torch.bfloat16)
+out = []
+for b_mn in (0, 1):
+    Bs = B.transpose(1, 2).contiguous() if b_mn else B
+    C = torch.zeros(G * Cs, N, device=dev, dtype=torch.bfloat16)
+    i32 = lambda v: torch.tensor(v, dtype=torch.int32, device=dev)
+    m, ar, b = i32(list(groups)), i32([g * Cs for g in range(G)]), i32(list(range(G)))
+    p = GemmProblem()
+    p.kind, p.epilogue = _lib.MOE_GEMM_RAGGED_M, _lib.MOE_EPI_STORE
+    p.dtype_ab = p.dtype_c = _lib.MOE_DTYPE_BF16
+    p.b_mn_major = b_mn
+    p.groups, p.N, p.K, p.a_rows, p.num_b = G, N, K, G * Cs, G
+    p.m, p.a_row, p.c_row, p.b = m.data_ptr(), ar.data_ptr(), ar.data_ptr(), b.data_ptr()
+    p.A, p.B, p.C, p.ldc = A.data_ptr(), Bs.data_ptr(), C.data_ptr(), N
+    grouped_gemm(p)
+    torch.cuda.synchronize()
+    out.append(C.cpu())
+torch.save(out, sys.argv[2])
+"""
+
+
+def test_multicast_clusters_bitwise_equal_pair_mode(tmp_path):
+    """The 2-pair multicast clusters (bf16 STORE GEMMs, preferred cluster
+    size 4) change only where the A rows come from: results are bitwise the
+    pair-mode ones (MOE_GEMM_MC=0), ragged groups, tails and empty groups
+    included, both B layouts."""
+    import os
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mc in ("0", "1"):
+        f = tmp_path / f"mc{mc}.pt"
+        env = dict(os.environ, MOE_GEMM_MC=mc)
+        subprocess.run([sys.executable, "-c", _MC_SCRIPT, repo, str(f)], env=env, check=True,
+                       timeout=300)
+        outs.append(torch.load(f))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    assert outs[1][0].abs().sum() > 0
