@@ -11,21 +11,15 @@
    runs over gloo; the arithmetic is the oracle's.
 """
 import os
-import socket
 
 import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
-import torch.multiprocessing as mp
+
+from mp_ranks import run_ranks
 
 
-def _port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
 
 
 def _worker(rank, world, port, q):
@@ -96,14 +90,4 @@ def _worker(rank, world, port, q):
 
 
 def test_ep_host_logic_world2_gloo():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=300) for _ in range(2)]
-    for p in procs:
-        p.join(timeout=60)
-    for r, msg in res:
-        assert msg == "ok", f"rank {r}:\n{msg}"
+    run_ranks(_worker, 2, timeout=300)

@@ -6,10 +6,11 @@ of the per-rank single-GPU gradients, gate gradients all-reduced.  Also the
 packed all-to-all itself (fused = 1 message per peer vs unfused slices) against
 alltoall_flat semantics (collectives.cpp:10-21)."""
 import os
-import socket
 
 import pytest
 import torch
+
+from mp_ranks import run_ranks
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
@@ -17,12 +18,6 @@ if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
     pytest.skip("needs >= 2 GPUs", allow_module_level=True)
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
 
 
 def _worker(rank, world, port, case, q):
@@ -216,18 +211,7 @@ def _worker(rank, world, port, case, q):
 
 
 def _run(case, world=2):
-    import torch.multiprocessing as mp
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=600) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=120)
-    for r, msg in res:
-        assert msg == "ok", f"rank {r}:\n{msg}"
+    run_ranks(_worker, world, (case,), timeout=600)
 
 
 def test_packed_alltoall_fused_and_unfused():

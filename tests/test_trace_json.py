@@ -3,13 +3,13 @@ writer/reader (workload.cpp:68-119, golden vectors from oracle/_ref), and the
 recorder's multi-rank gather over gloo (world_size 2)."""
 import json
 import os
-import socket
 
 import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
-import torch.multiprocessing as mp
+
+from mp_ranks import run_ranks
 
 import oracle
 from paper_2205_10034_b200 import moesim
@@ -46,12 +46,6 @@ def test_trace_from_json_errors_match_reference(ent):
         assert tr.tokens_per_rank == exp["tokens_per_rank"]
 
 
-def _port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
 
 
 def _worker(rank, world, port, q):
@@ -71,15 +65,7 @@ def _worker(rank, world, port, q):
 
 
 def test_recorder_gathers_ranks_in_order():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in ps:
-        p.start()
-    out = dict(q.get(timeout=120) for _ in ps)
-    for p in ps:
-        p.join(timeout=60)
+    out = run_ranks(_worker, 2, timeout=120, is_ok=lambda m: m.startswith("{"))
     assert out[0] == out[1], out
     tr = moesim.trace_from_json(out[0])  # validates row sums = k*T
     assert (tr.steps, tr.ranks, tr.experts, tr.tokens_per_rank) == (3, 2, 4, 20)
