@@ -108,6 +108,10 @@ def main():
         ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
         scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
         seq = [(short(r[ki])[0], fnum(r[vi]) * scale.get(r[ui], 1.0)) for r in rows[1:]]
+        # our kernels only: drop torch's and the cuBLAS reference GEMMs the
+        # bench times after the steps (roofline.cublas_dense_equivalent)
+        lib = ("nvjet", "cublas", "cutlass", "sm90_", "sm100_", "at::", "void at::")
+        seq = [(n, t) for n, t in seq if not n.startswith(lib) and "at::native" not in n]
         # the last full step: from the last gate-logits GEMM (first launch of
         # a step) on, our kernels only
         starts = [i for i, (n, _) in enumerate(seq) if n.endswith("<64, 0, 0, 0, 0, 1, 1, 0>")]
