@@ -121,6 +121,68 @@ __global__ void __launch_bounds__(256) finish_kernel(
   if (out3) split3_store4(h, out3, n3, off);
 }
 
+// MODE 2 (dH = h * gelu') with the bias gradient db1 fused: a block owns 32
+// rows (a warp 4 consecutive rows) x 128 columns of one group and writes the
+// column sums of its 32 stored rows (rows >= m are zero) to
+// cs_part[(g * maxch + row block) * N + n] -- the 32-row chunk partials
+// seg_colsum sums in chunk order (deterministic), instead of a separate
+// column-sum pass re-reading dH.
+__global__ void __launch_bounds__(256) finish_dgelu_cs_kernel(
+    const float* __restrict__ part, int nparts, uint64_t pstride, const int32_t* __restrict__ gm,
+    const int32_t* __restrict__ ga, int stride, int N, const float* __restrict__ aux,
+    float* __restrict__ out, __nv_bfloat16* __restrict__ out3, uint64_t n3,
+    float* __restrict__ cs_part, int maxch) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float4 red[8][32];
+  const int g = blockIdx.x;
+  const int m = gm[g];
+  const int lim = min(stride, (m + 63) & ~63);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = (blockIdx.z * 32 + lane) * 4;
+  float4 cs = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = blockIdx.y * 32 + w * 4 + i;
+    if (r >= lim || n >= N) continue;
+    const uint64_t off = ((uint64_t)ga[g] + r) * N + n;
+    float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < m) {
+      for (int c = 0; c < nparts; ++c) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(part + (uint64_t)c * pstride + off));
+        h.x += v.x;
+        h.y += v.y;
+        h.z += v.z;
+        h.w += v.w;
+      }
+      const float4 x = __ldg(reinterpret_cast<const float4*>(aux + off));
+      h.x *= x.x;
+      h.y *= x.y;
+      h.z *= x.z;
+      h.w *= x.w;
+    }
+    if (out) *reinterpret_cast<float4*>(out + off) = h;
+    if (out3) split3_store4(h, out3, n3, off);
+    cs.x += h.x;
+    cs.y += h.y;
+    cs.z += h.z;
+    cs.w += h.w;
+  }
+  red[w][lane] = cs;
+  __syncthreads();
+  if (w == 0 && n < N && blockIdx.y < (unsigned)maxch) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) {
+      t.x += red[k][lane].x;
+      t.y += red[k][lane].y;
+      t.z += red[k][lane].z;
+      t.w += red[k][lane].w;
+    }
+    *reinterpret_cast<float4*>(cs_part + ((uint64_t)g * maxch + blockIdx.y) * N + n) = t;
+  }
+}
+
 // K-chunk group tables, group (c, g) = c * groups + g:
 //   RAGGED_M (kind 0): m = gm, a_row = ga, c_row = c * rows + ga, b = gb, k = c * chunk
 //   RAGGED_K (kind 1): m = clamp(gm - c*chunk, 0, chunk), a_row = ga + c*chunk, b = c*nb + gb
@@ -181,6 +243,21 @@ void split_finish(int mode, const float* part, int nparts, uint64_t part_stride,
                (int)stride, (int)N, bias, aux, out, out2, o3, n3);
   MOE_LAUNCH_CHECK("finish_kernel");
   count_launch();
+}
+
+void split_finish_dgelu_colsum(const float* part, int nparts, uint64_t part_stride,
+                               uint32_t groups, const int32_t* gm, const int32_t* ga,
+                               const int32_t* gb, uint32_t num_b, uint32_t stride, uint32_t N,
+                               const float* aux, float* out, void* out3, uint64_t n3,
+                               float* cs_part, float* db, cudaStream_t st) {
+  arg_check(N % 4 == 0, "split_finish: N % 4 == 0 required");
+  const int maxch = (int)ceil_div((uint64_t)stride, (uint64_t)32);
+  const dim3 grid(groups, (unsigned)maxch, (unsigned)ceil_div((uint64_t)N, (uint64_t)128));
+  launch_pdl(finish_dgelu_cs_kernel, grid, 256, 0, st, part, nparts, part_stride, gm, ga,
+             (int)stride, (int)N, aux, out, static_cast<__nv_bfloat16*>(out3), n3, cs_part, maxch);
+  MOE_LAUNCH_CHECK("finish_dgelu_cs_kernel");
+  count_launch();
+  seg_colsum(groups, gm, gb, num_b, N, 32, (uint32_t)maxch, cs_part, db, st);
 }
 
 void chunk_tables(int kind, uint32_t groups, int nchunks, int chunk, int rows, int nb,

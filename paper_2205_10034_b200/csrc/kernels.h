@@ -137,6 +137,14 @@ inline uint64_t gemm_colsum_ws_floats(uint32_t groups, uint32_t N, uint64_t max_
 // (mode 0: + bias; 1: GeLU / GeLU' of (sum + bias) into out / out2; 2: sum x
 // aux) over the rows of each group, pad rows [m, stride) zeroed.
 void split_f32_bf16x3(const float* in, uint64_t n, void* out, cudaStream_t st);
+// MODE 2 with the bias gradient fused: db[gb[g]] = column sums of the stored
+// rows (32-row chunk partials in cs_part [groups][ceil(stride/32)][N], then
+// seg_colsum in chunk order)
+void split_finish_dgelu_colsum(const float* part, int nparts, uint64_t part_stride,
+                               uint32_t groups, const int32_t* gm, const int32_t* ga,
+                               const int32_t* gb, uint32_t num_b, uint32_t stride, uint32_t N,
+                               const float* aux, float* out, void* out3, uint64_t n3,
+                               float* cs_part, float* db, cudaStream_t st);
 void split_finish(int mode, const float* part, int nparts, uint64_t part_stride, uint32_t groups,
                   const int32_t* gm, const int32_t* ga, const int32_t* gb, uint32_t stride,
                   uint32_t N, const float* bias, const float* aux, float* out, float* out2,

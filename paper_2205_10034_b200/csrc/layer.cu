@@ -667,10 +667,11 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p.B = w2_3;
     p.ldc = dff;
     split_gemm(p, s_part, rows * dff, &np, st);
-    split_finish(2, s_part, np, rows * dff, ngroups, gm, ga, gb, (uint32_t)gstride, dff, nullptr,
-                 static_cast<const float*>(Gp), static_cast<float*>(dH), nullptr, dh3, rows * dff,
-                 st);
-    group_colsum(ngroups, gm, ga, gb, El, dff, dt, dH, g.db1, st, gstride, s_cs, nullptr);
+    // dH = h * gelu'(h) to its bf16 planes (dgrad-ffn1's / wgrad-w1's operand)
+    // and db1 = its column sums (chunk partials in s_cs, fixed-order sum)
+    split_finish_dgelu_colsum(s_part, np, rows * dff, ngroups, gm, ga, gb, El, (uint32_t)gstride,
+                              dff, static_cast<const float*>(Gp), nullptr, dh3, rows * dff, s_cs,
+                              g.db1, st);
     mark("dgrad_ffn2", st);
     p = expert_problem();
     p.b_mn_major = 1;
