@@ -121,13 +121,16 @@ __global__ void __launch_bounds__(256) finish_kernel(
   if (out3) split3_store4(h, out3, n3, off);
 }
 
-// MODE 2 (dH = h * gelu') with the bias gradient db1 fused: a block owns 32
-// rows (a warp 4 consecutive rows) x 128 columns of one group and writes the
-// column sums of its 32 stored rows (rows >= m are zero) to
-// cs_part[(g * maxch + row block) * N + n] -- the 32-row chunk partials
-// seg_colsum sums in chunk order (deterministic), instead of a separate
-// column-sum pass re-reading dH.
-__global__ void __launch_bounds__(256) finish_dgelu_cs_kernel(
+// Planes + bias gradient in one pass: a block owns 32 rows (a warp 4
+// consecutive rows) x 128 columns of one group, computes the rows' values --
+// SRC 0: dH = (sum of the K-chunk partials) * gelu' (MODE 2 of finish_kernel);
+// SRC 1: a plain fp32 input (dY) -- stores their three bf16 planes (and fp32,
+// if `out`), and writes the column sums of its 32 rows (rows >= m are zero)
+// to cs_part[(g * maxch + row block) * N + n]: the 32-row chunk partials
+// seg_colsum sums in chunk order (deterministic) -- instead of a separate
+// column-sum pass re-reading the values (db1 / db2).
+template <int SRC>
+__global__ void __launch_bounds__(256) planes_colsum_kernel(
     const float* __restrict__ part, int nparts, uint64_t pstride, const int32_t* __restrict__ gm,
     const int32_t* __restrict__ ga, int stride, int N, const float* __restrict__ aux,
     float* __restrict__ out, __nv_bfloat16* __restrict__ out3, uint64_t n3,
@@ -147,7 +150,9 @@ __global__ void __launch_bounds__(256) finish_dgelu_cs_kernel(
     if (r >= lim || n >= N) continue;
     const uint64_t off = ((uint64_t)ga[g] + r) * N + n;
     float4 h = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (r < m) {
+    if (r < m && SRC == 1) {
+      h = __ldcg(reinterpret_cast<const float4*>(part + off));
+    } else if (r < m) {
       for (int c = 0; c < nparts; ++c) {
         const float4 v = __ldcg(reinterpret_cast<const float4*>(part + (uint64_t)c * pstride + off));
         h.x += v.x;
@@ -253,9 +258,22 @@ void split_finish_dgelu_colsum(const float* part, int nparts, uint64_t part_stri
   arg_check(N % 4 == 0, "split_finish: N % 4 == 0 required");
   const int maxch = (int)ceil_div((uint64_t)stride, (uint64_t)32);
   const dim3 grid(groups, (unsigned)maxch, (unsigned)ceil_div((uint64_t)N, (uint64_t)128));
-  launch_pdl(finish_dgelu_cs_kernel, grid, 256, 0, st, part, nparts, part_stride, gm, ga,
+  launch_pdl(planes_colsum_kernel<0>, grid, 256, 0, st, part, nparts, part_stride, gm, ga,
              (int)stride, (int)N, aux, out, static_cast<__nv_bfloat16*>(out3), n3, cs_part, maxch);
-  MOE_LAUNCH_CHECK("finish_dgelu_cs_kernel");
+  MOE_LAUNCH_CHECK("planes_colsum_kernel");
+  count_launch();
+  seg_colsum(groups, gm, gb, num_b, N, 32, (uint32_t)maxch, cs_part, db, st);
+}
+
+void split_colsum_f32(const float* in, uint32_t groups, const int32_t* gm, const int32_t* ga,
+                      const int32_t* gb, uint32_t num_b, uint32_t stride, uint32_t N, void* out3,
+                      uint64_t n3, float* cs_part, float* db, cudaStream_t st) {
+  arg_check(N % 4 == 0, "split_colsum: N % 4 == 0 required");
+  const int maxch = (int)ceil_div((uint64_t)stride, (uint64_t)32);
+  const dim3 grid(groups, (unsigned)maxch, (unsigned)ceil_div((uint64_t)N, (uint64_t)128));
+  launch_pdl(planes_colsum_kernel<1>, grid, 256, 0, st, in, 1, (uint64_t)0, gm, ga, (int)stride,
+             (int)N, nullptr, nullptr, static_cast<__nv_bfloat16*>(out3), n3, cs_part, maxch);
+  MOE_LAUNCH_CHECK("planes_colsum_kernel");
   count_launch();
   seg_colsum(groups, gm, gb, num_b, N, 32, (uint32_t)maxch, cs_part, db, st);
 }

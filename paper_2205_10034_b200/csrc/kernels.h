@@ -145,6 +145,11 @@ void split_finish_dgelu_colsum(const float* part, int nparts, uint64_t part_stri
                                const int32_t* gb, uint32_t num_b, uint32_t stride, uint32_t N,
                                const float* aux, float* out, void* out3, uint64_t n3,
                                float* cs_part, float* db, cudaStream_t st);
+// fp32 rows -> their three bf16 planes, and db = column sums of each group's
+// rows (same chunk partials + seg_colsum); rows past round_up(m, 64) untouched
+void split_colsum_f32(const float* in, uint32_t groups, const int32_t* gm, const int32_t* ga,
+                      const int32_t* gb, uint32_t num_b, uint32_t stride, uint32_t N, void* out3,
+                      uint64_t n3, float* cs_part, float* db, cudaStream_t st);
 void split_finish(int mode, const float* part, int nparts, uint64_t part_stride, uint32_t groups,
                   const int32_t* gm, const int32_t* ga, const int32_t* gb, uint32_t stride,
                   uint32_t N, const float* bias, const float* aux, float* out, float* out2,

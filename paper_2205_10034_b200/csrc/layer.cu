@@ -596,8 +596,12 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   // db2 = column sums of dY, while dY is still warm in L2 (after the weight
   // gradients the L2 is full of dirty fp32 dW lines and every read pays a
   // write-back)
-  group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs,
-               cs_part, cs_ticket);
+  if (split32)  // + dY's bf16 planes (dgrad-ffn2's / wgrad-w2's operand) in the same pass
+    split_colsum_f32(static_cast<const float*>(dYr), ngroups, gm, ga, gb, El, (uint32_t)gstride,
+                     dm, dy3, rows * dm, cs_part, g.db2, st);
+  else
+    group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs,
+                 cs_part, cs_ticket);
   mark("bias_grads", st);
   // Weight-gradient GEMMs (RAGGED_K over the slices of each expert):
   // dW1[j] = sum dH^T X, dW2[j] = sum dY^T A.
@@ -657,8 +661,7 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
   // dXe = dH W1
   const bool fused_return = p2p && dt == MOE_DTYPE_BF16;
   if (split32) {
-    int np = 0;
-    split_f32_bf16x3(static_cast<const float*>(dYr), rows * dm, dy3, st);
+    int np = 0;  // dy3: dY's planes, written with db2 (bias_grads)
     moe_gemm_problem_t p = expert_problem();
     p.b_mn_major = 1;
     p.N = dff;
