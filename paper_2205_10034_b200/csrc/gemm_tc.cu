@@ -59,17 +59,26 @@ struct Cfg {
   // DGELU: aux tile (TMA, double-buffered); GATHER_ADD: 2 gathered sources x
   // the 4 chunks of a warp's tile (all prefetched when the tile starts)
   static constexpr int NAUX = (EPI == MOE_EPI_DGELU) ? 2 : (EPI == MOE_EPI_GATHER_ADD ? 8 : 0);
-  // output staging buffers per warp: double-buffered (the TMA store of chunk c
-  // drains while chunk c+1 is computed) where the epilogue is the long pole
-  // -- except the weight gradients (RAGGED_K): single-buffered, and no bias
-  // slice, so the freed shared memory buys a sixth operand stage for their
-  // MN-major loads (A/B on c2: wgrad 0.50 -> 0.45 ms; the MMA warp was waiting
-  // on operands, not on the epilogue)
+  // output staging buffers per warp: single-buffered (the TMA store of chunk
+  // c must have read the buffer before chunk c+1 is staged) for the expert
+  // GEMMs -- the freed shared memory buys operand stages, and these kernels
+  // wait on operands (per-expert weights from DRAM), not on the epilogue:
+  // weight gradients 5 -> 6 stages (A/B on c2: 0.50 -> 0.45 ms), GeLU /
+  // GeLU' epilogues 4 -> 5 stages (round 2: c2 step -1.1%, c3 -0.9%, 3+3
+  // interleaved runs); double-buffered only for the fp32-output ones
 #ifndef MOE_WGRAD_NBUF
 #define MOE_WGRAD_NBUF 1
 #endif
+#ifndef MOE_GELU_NBUF
+#define MOE_GELU_NBUF 1
+#endif
+#ifndef MOE_DGELU_NBUF
+#define MOE_DGELU_NBUF 1
+#endif
   static constexpr int NBUF = KIND == 1 && EPI == MOE_EPI_STORE ? MOE_WGRAD_NBUF
-                              : (EPI == MOE_EPI_GELU || EPI == MOE_EPI_DGELU || CF32) ? 2 : 1;
+                              : EPI == MOE_EPI_GELU ? MOE_GELU_NBUF
+                              : EPI == MOE_EPI_DGELU ? MOE_DGELU_NBUF
+                              : CF32 ? 2 : 1;
   // + the warp's bias slice of the current tile (STORE/GELU): BN/2 floats
   static constexpr int BIAS_BYTES =
       KIND == 0 && (EPI == MOE_EPI_STORE || EPI == MOE_EPI_GELU) ? BN * 2 : 0;
