@@ -1,14 +1,17 @@
 // K5 — grouped expert GEMM on 5th-generation tensor cores (sm_100a).
 //
-// One persistent, warp-specialised kernel per shape class (384 threads):
-//   warp 0       TMA producer (one lane): A/B tiles -> 128B-swizzled smem ring
-//   warp 1       MMA issuer  (one lane): tcgen05.mma 128xBNx16, fp32 accum in TMEM
-//   warp 2       TMEM allocator (2 x BN columns: double-buffered accumulator)
-//   warps 4..11  epilogue: warp w owns TMEM lanes 32*(w%4).. and half the columns;
+// One persistent, warp-specialised kernel per shape class (384 threads; CTA
+// pairs, cta_group::2, for the expert GEMMs -- 2-pair multicast clusters for
+// the bf16 STORE ones):
+//   warps 0..7   epilogue: warp w owns TMEM lanes 32*(w%4).. and half the columns;
 //                tcgen05.ld -> bias / GeLU / GeLU' / gather-add -> bf16|fp32 ->
 //                64B-swizzled smem staging -> TMA bulk tensor store (partial
 //                row blocks fall back to masked stores); GeLU' operands arrive
 //                by TMA one chunk ahead; optional fused column sums (bias grad).
+//   warp 8       TMA producer (one lane): A/B tiles -> 128B-swizzled smem ring
+//   warp 9       MMA issuer (pair leader): tcgen05.mma 256xBNx16, fp32 accum in TMEM
+//   warp 10      TMEM allocator (2 x BN columns: double-buffered accumulator)
+//   warp 11      group-table scan (tiles per group -> prefix sums in smem)
 // Work items come from device-side group tables (no host sync on routing
 // counts — the paper's CPU-side scheduling overhead):
 //   RAGGED_M : group g = one (source, expert) slice of m[g] rows; tiles =
