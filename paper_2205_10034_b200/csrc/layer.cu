@@ -246,6 +246,12 @@ Layer::Layer(const moe_layer_desc_t& d) : desc(d) {
 
 Layer::~Layer() {
   if (p2p) p2p_teardown(win);  // device sync + BYE handshake, then unmap / free
+  if (bw_side) {
+    cudaStreamSynchronize(bw_side);
+    cudaStreamDestroy(bw_side);
+    cudaEventDestroy(bw_fork);
+    cudaEventDestroy(bw_join);
+  }
   for (auto& lg : plog)
     for (int i = 0; i < kMaxPhases + 1; ++i) cudaEventDestroy(lg.ev[i]);
   for (void* p : owned) cudaFree(p);
@@ -523,6 +529,15 @@ void Layer::forward(const moe_layer_params_t& w, const void* x, void* y, const f
   has_forward = true;
 }
 
+// MOE_BWD_FORK=0 keeps the backward on one stream (A/B switch)
+static bool bwd_fork_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MOE_BWD_FORK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, void* dx,
                      const moe_layer_grads_t& g, cudaStream_t st) {
   require(has_forward, MOE_ERR_LOGIC, "backward: no forward pass recorded on this layer");
@@ -542,6 +557,44 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     combine_backward(T, dm, E, k, C, pad, dt, dy, Yh, slot, gate, dkept(), dYs, dgate, st);
   }
   mark("combine_bwd", st);
+  // The received dY and its column sums (db2) do not depend on the routing
+  // backward / gate weight gradient: with the fork on they run on a side
+  // stream beside them (two short memory-bound chains overlap instead of
+  // queueing), joined before dgrad-ffn2.  Not for the NCCL exchange (its
+  // collectives stay on one stream) and not in profiled steps (phases stay
+  // attributable).
+  const bool fork = bwd_fork_enabled() && (p2p || P == 1) && !profiling;
+  cudaStream_t sd = st;
+  auto dy_and_db2 = [&](cudaStream_t s) {
+    if (p2p) {
+      p2p_wait(win, SLOT_DY, ph, s);
+      p2p_local_groups(win, gm, ga, gb, dYr, s);  // zero the K-block pad rows of recv_dy
+    }
+    else if (P > 1) a2a(dYs, dYr, El * Cs * dm * esz, s);
+    mark("a2a_dy", s);
+    // db2 = column sums of dY, while dY is still warm in L2 (after the weight
+    // gradients the L2 is full of dirty fp32 dW lines and every read pays a
+    // write-back)
+    if (split32)  // + dY's bf16 planes (dgrad-ffn2's / wgrad-w2's operand) in the same pass
+      split_colsum_f32(static_cast<const float*>(dYr), ngroups, gm, ga, gb, El, (uint32_t)gstride,
+                       dm, dy3, rows * dm, cs_part, g.db2, s);
+    else
+      group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, s, p2p ? (uint64_t)P * Cs : Cs,
+                   cs_part, cs_ticket);
+    mark("bias_grads", s);
+  };
+  if (fork) {
+    if (!bw_side) {
+      MOE_CUDA(cudaStreamCreateWithFlags(&bw_side, cudaStreamNonBlocking));
+      MOE_CUDA(cudaEventCreateWithFlags(&bw_fork, cudaEventDisableTiming));
+      MOE_CUDA(cudaEventCreateWithFlags(&bw_join, cudaEventDisableTiming));
+    }
+    sd = bw_side;
+    MOE_CUDA(cudaEventRecord(bw_fork, st));
+    MOE_CUDA(cudaStreamWaitEvent(sd, bw_fork, 0));
+    dy_and_db2(sd);
+    MOE_CUDA(cudaEventRecord(bw_join, sd));
+  }
   // K2^T: dlogits (and dbg, summed over token blocks in a fixed order)
   route_backward(T, E, k, logits, expert, gate, keep, count1, dgate, d_aux, dl_f32, dl_lp,
                  dt == MOE_DTYPE_BF16 ? MOE_DTYPE_BF16 : MOE_DTYPE_F32,
@@ -587,22 +640,8 @@ void Layer::backward(const moe_layer_params_t& w, const void* dy, float d_aux, v
     p2p_allreduce_push(win, g.dwg, (uint64_t)E * dm, desc.has_gate_bias ? g.dbg : nullptr,
                        desc.has_gate_bias && g.dbg ? E : 0, ph, st);
   mark("gate_wgrad", st);
-  if (p2p) {
-    p2p_wait(win, SLOT_DY, ph, st);
-    p2p_local_groups(win, gm, ga, gb, dYr, st);  // zero the K-block pad rows of recv_dy
-  }
-  else if (P > 1) a2a(dYs, dYr, El * Cs * dm * esz, st);
-  mark("a2a_dy", st);
-  // db2 = column sums of dY, while dY is still warm in L2 (after the weight
-  // gradients the L2 is full of dirty fp32 dW lines and every read pays a
-  // write-back)
-  if (split32)  // + dY's bf16 planes (dgrad-ffn2's / wgrad-w2's operand) in the same pass
-    split_colsum_f32(static_cast<const float*>(dYr), ngroups, gm, ga, gb, El, (uint32_t)gstride,
-                     dm, dy3, rows * dm, cs_part, g.db2, st);
-  else
-    group_colsum(ngroups, gm, ga, gb, El, dm, dt, dYr, g.db2, st, p2p ? (uint64_t)P * Cs : Cs,
-                 cs_part, cs_ticket);
-  mark("bias_grads", st);
+  if (fork) MOE_CUDA(cudaStreamWaitEvent(st, bw_join, 0));
+  else dy_and_db2(st);
   // Weight-gradient GEMMs (RAGGED_K over the slices of each expert):
   // dW1[j] = sum dH^T X, dW2[j] = sum dY^T A.
   auto wgrad = [&](bool w1, cudaStream_t s) {

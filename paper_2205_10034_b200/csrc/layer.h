@@ -105,6 +105,8 @@ struct Layer {
   const void* x_saved_ptr = nullptr;
   void* x_stage = nullptr;          // host-buffer pipeline: 2 x (x, dy, y, dx)
   cudaStream_t hp_stream[3] = {};   // h2d, compute, d2h
+  cudaStream_t bw_side = nullptr;    // backward: dY receipt + db2 beside the routing backward
+  cudaEvent_t bw_fork = nullptr, bw_join = nullptr;
   // per stage: x landed, dy landed, forward done, backward done, d2h done
   cudaEvent_t hp_ev[2][5] = {};
   cudaEvent_t hp_entry = nullptr;   // caller-stream state at each train_step_host entry
