@@ -69,7 +69,10 @@ __global__ void __launch_bounds__(GT) gate_logits_f32_kernel(uint64_t T, int d, 
 // Block: TOKC tokens x 64 columns; thread (col = tid % 64, eg = tid / 64)
 // accumulates experts e = eg + 4 j over the chunk and stores the chunk's
 // partial; the chunks are summed in order afterwards (deterministic).
-constexpr int TOKC = 128;
+// 32-token chunks: 4x the blocks of 128-token ones (c1: 1024 instead of 256,
+// the per-thread token loop was latency-bound); their partials are summed in
+// chunk order by sum_parts
+constexpr int TOKC = kGateWgradTok;
 template <int NE>
 __global__ void __launch_bounds__(GT) gate_wgrad_f32_kernel(uint64_t T, int d, int E,
                                                             const float* __restrict__ dl,
@@ -139,15 +142,31 @@ __global__ void __launch_bounds__(GT) gate_dx_f32_kernel(uint64_t T, int d, int 
     for (int i = 0; i < DX_TOK / 4; ++i) acc[i] = fmaf(dls[(tg + 4 * i) * (E + 1) + e], w, acc[i]);
   }
   if (col >= d) return;
+  // every routing slot of the thread's tokens first, then every gathered
+  // row element (16 independent loads in flight instead of a chain per token),
+  // then the sums in the same order as before (acc + row 0 + row 1)
+  constexpr int NT = DX_TOK / 4;
+  int32_t sl[NT][2];
 #pragma unroll
-  for (int i = 0; i < DX_TOK / 4; ++i) {
+  for (int i = 0; i < NT; ++i) {
+    const uint64_t t = t0 + tg + 4 * i;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) sl[i][j] = (t < T && j < k) ? slot[t * k + j] : -1;
+  }
+  float gv[NT][2];
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      gv[i][j] = sl[i][j] >= 0 ? __ldg(dXe + (uint64_t)sl[i][j] * d + col) : 0.f;
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
     const uint64_t t = t0 + tg + 4 * i;
     if (t >= T) break;
     float v = acc[i];
-    for (int j = 0; j < k; ++j) {
-      const int32_t s = slot[t * k + j];
-      if (s >= 0) v += dXe[(uint64_t)s * d + col];
-    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (sl[i][j] >= 0) v += gv[i][j];
     dx[t * d + col] = v;
   }
 }
@@ -201,6 +220,7 @@ void gate_dx_f32(uint64_t T, uint32_t d, uint32_t E, uint32_t k, const float* dl
                  const float* dXe, const int32_t* slot, float* dx, cudaStream_t st) {
   if (!T) return;
   arg_check(E >= 1 && E <= 256, "gate_dx_f32: E must be in [1, 256]");
+  arg_check(k >= 1 && k <= 2, "gate_dx_f32: k must be 1 or 2");
   const size_t smem = sizeof(float) * (E * 64 + DX_TOK * (E + 1));
   if (smem > 48 * 1024)
     MOE_CUDA(cudaFuncSetAttribute(gate_dx_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

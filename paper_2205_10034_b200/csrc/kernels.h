@@ -94,8 +94,9 @@ void gate_logits_f32(uint64_t T, uint32_t d, uint32_t E, const float* x, const f
                      const float* bg, float* logits, cudaStream_t st);
 void gate_wgrad_f32(uint64_t T, uint32_t d, uint32_t E, const float* dl, const float* x,
                     float* dwg, float* ws, cudaStream_t st);
+constexpr int kGateWgradTok = 32;  // tokens per gate_wgrad_f32 block (one partial each)
 inline uint64_t gate_wgrad_f32_ws_floats(uint64_t T, uint32_t d, uint32_t E) {
-  return ((T + 127) / 128) * (uint64_t)E * d;
+  return ((T + kGateWgradTok - 1) / kGateWgradTok) * (uint64_t)E * d;
 }
 void gate_dx_f32(uint64_t T, uint32_t d, uint32_t E, uint32_t k, const float* dl, const float* wg,
                  const float* dXe, const int32_t* slot, float* dx, cudaStream_t st);
