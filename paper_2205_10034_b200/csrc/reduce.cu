@@ -81,13 +81,39 @@ __global__ void __launch_bounds__(RT) seg_colsum_kernel(uint32_t groups, const i
   pdl_trigger();
   constexpr int V = VEC ? 4 : 1;
   __shared__ float4 red[PW][32];
+  __shared__ int glist[1024];  // this output's groups, ascending
+  __shared__ int wcnt[PW], gtotal;
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // ordered compaction of {g : gb[g] == b} by the whole block (ballots + a
+  // prefix over the warps per 256-group slice) instead of every warp walking
+  // all groups (c2: 64 dependent checks per warp, ~90% of this kernel's
+  // instructions); the summation order below is unchanged (ascending g)
+  if (threadIdx.x == 0) gtotal = 0;
+  __syncthreads();
+  for (uint32_t g0 = 0; g0 < groups; g0 += RT) {
+    const uint32_t g = g0 + threadIdx.x;
+    const bool mine = g < groups && __ldg(gb + g) == b;
+    const uint32_t bal = __ballot_sync(0xffffffffu, mine);
+    if (lane == 0) wcnt[w] = __popc(bal);
+    __syncthreads();
+    int base = gtotal;
+    for (int k = 0; k < w; ++k) base += wcnt[k];
+    if (mine) glist[base + __popc(bal & ((1u << lane) - 1u))] = (int)g;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int k = 0; k < PW; ++k) t += wcnt[k];
+      gtotal += t;
+    }
+    __syncthreads();
+  }
+  const int ng = gtotal;
   const uint32_t n = (blockIdx.y * 32 + lane) * V;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (n < N) {
-    for (uint32_t g = 0; g < groups; ++g) {
-      if (__ldg(gb + g) != b) continue;
+    for (int gi = 0; gi < ng; ++gi) {
+      const uint32_t g = (uint32_t)glist[gi];
       const int nch = min((int)maxch, (__ldg(gm + g) + (int)chunk - 1) / (int)chunk);
       const float* p = ws + (uint64_t)g * maxch * N + n;
       auto ld = [&](int ch) -> float4 {
